@@ -1,0 +1,118 @@
+/*
+ * halftime_b200.h -- C-ABI of the B200-native HalftimeHash engine
+ * (libhalftime_b200.so).  Plain pointers and sizes only; no torch types.
+ *
+ * The reference (halftimehash 0.1.0, /root/reference/pkg/src/halftimehash)
+ * is a pure-Python package with no FFI.  Its only plug-in point is the
+ * `engine` string of `hash_bytes` (hasher.py:434-453); each entry point
+ * below is what that dispatch (and the batched seam `_hash_words_np`,
+ * hasher.py:331-413) would bind through ctypes.  INTEGRATION.md shows the
+ * binding a maintainer would add.
+ *
+ * Conventions
+ *  - Return 0 on success or a negative HTH_E* code; the message is in
+ *    hth_last_error() (thread-local).  Never aborts.
+ *  - Error mapping to the reference's exceptions:
+ *      HTH_EINVAL    -> ValueError   (unsupported width params.py:230-237,
+ *                                     bad master hasher.py:48-50, bad args)
+ *      HTH_ESEEDSIZE -> SeedSizeError (hasher.py:36-37, 209-214)
+ *      HTH_ERANGE    -> IndexError    (hasher.py:84-97)
+ *      HTH_ECUDA / HTH_ENOMEM -> RuntimeError / MemoryError
+ *  - Device entry points are stream-ordered on `stream` (a cudaStream_t,
+ *    NULL = legacy default stream) and asynchronous.
+ *  - Device input buffers must be 16-byte aligned at their base and
+ *    readable up to the next 16-byte boundary past their last byte (TMA
+ *    bulk copies move 16-byte granules).  Any cudaMalloc / torch
+ *    allocation satisfies this.
+ *  - Digests are written as n_strings x k little-endian u64 words,
+ *    k = output_bytes / 8 (Digest.words, hasher.py:165-176).
+ *  - Seeds: d_seed holds the expanded seed words S[0..seed_capacity)
+ *    (SeedBuffer.words_np, hasher.py:94-97).  Any capacity >= the layout
+ *    total is accepted and gives identical digests (hasher.py:8-10).
+ */
+#ifndef HALFTIME_B200_H
+#define HALFTIME_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HTH_OK 0
+#define HTH_EINVAL (-1)
+#define HTH_ESEEDSIZE (-2)
+#define HTH_ERANGE (-3)
+#define HTH_ECUDA (-4)
+#define HTH_ENOMEM (-5)
+
+/* Last error message of the calling thread ("" if none). */
+const char* hth_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int hth_version(void);
+
+/* params.variant(output_bytes) geometry (params.py:133-237): k, e, d, w and
+ * words per instance m = d*w*8.  HTH_EINVAL for widths other than 16/24/32/40. */
+int hth_variant_geometry(int output_bytes, int* k, int* e, int* d, int* w, int* instance_words);
+
+/* seed_words_needed(params, n_bytes)  (hasher.py:156-158). */
+int hth_seed_words_needed(int output_bytes, uint64_t n_bytes, uint64_t* out_words);
+
+/* seed_layout(params, n_bytes)  (hasher.py:130-153) as 10 words:
+ * levels, ehc_start, ehc_words, tree_start, tree_words_per_tree,
+ * finalize_start, finalize_words_per_tree, remainder_start, remainder_words,
+ * total_words. */
+int hth_seed_layout(int output_bytes, uint64_t n_bytes, uint64_t out10[10]);
+
+/* _master_fold (hasher.py:48-52): XOR of the four LE u64 of a 32-byte master. */
+int hth_master_fold(const uint8_t master[32], uint64_t* fold);
+
+/* SeedBuffer.words_np(start, count) on the device  (hasher.py:55-67, 94-97):
+ * d_words[i] = mix(fold + (start + i + 1) * 0x9E3779B97F4A7C15). */
+int hth_expand_seed(uint64_t fold, uint64_t start, uint64_t count, uint64_t* d_words, void* stream);
+
+/* cli.fill_bytes (cli.py:48-53) on the device: n_bytes of the splitmix stream
+ * keyed by fill_seed, starting at stream word `word_offset`. */
+int hth_fill_splitmix(uint64_t fill_seed, uint64_t word_offset, uint64_t n_bytes, void* d_dst, void* stream);
+
+/* ---- batched hash of equal-length strings: the _hash_words_np seam
+ *      (hasher.py:331-413) for B = n_strings rows sharing n_bytes.
+ * String s starts at d_data + s * stride_bytes.  Workspace: at least
+ * hth_workspace_size_fixed() bytes of device memory (NULL if that is 0). */
+int hth_workspace_size_fixed(int output_bytes, uint64_t n_strings, uint64_t n_bytes, uint64_t* bytes);
+int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uint64_t stride_bytes,
+                   uint64_t n_bytes, const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out,
+                   void* d_workspace, uint64_t workspace_bytes, void* stream);
+
+/* ---- batched hash of variable-length strings packed in one buffer.
+ * String s is d_data[d_offsets[s] .. d_offsets[s+1]) (u64 byte offsets on the
+ * device, any alignment).  max_n_bytes: an upper bound on any string's
+ * length, checked against seed_capacity on the host (SeedSizeError); strings
+ * longer than it are flagged (hth_varlen_status).  total_bytes sizes the
+ * workspace (>= d_offsets[n] - d_offsets[0]). */
+int hth_workspace_size_varlen(int output_bytes, uint64_t n_strings, uint64_t total_bytes, uint64_t* bytes);
+int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offsets, uint64_t n_strings,
+                    uint64_t max_n_bytes, uint64_t total_bytes, const uint64_t* d_seed, uint64_t seed_capacity,
+                    uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes, void* stream);
+/* Synchronizes `stream`; returns HTH_ESEEDSIZE if the last varlen call on this
+ * workspace met a string longer than its max_n_bytes, else HTH_OK. */
+int hth_varlen_status(void* d_workspace, void* stream);
+
+/* ---- host-buffer entry points (end-to-end; synchronous).  These are what
+ * hash_bytes(..., engine="cuda") binds: host bytes in, host digest words
+ * out, seeds expanded on the device from the 32-byte master.  The batch
+ * form pipelines host->device copies against hashing in chunks on two
+ * streams; pinned (page-locked) h_data gives full PCIe/NVLink-C2C rate.
+ * seed_capacity emulates SeedBuffer.capacity: HTH_ESEEDSIZE if it is below
+ * seed_words_needed (0 = size it exactly, like seed_for_input). */
+int hth_hash_host(int output_bytes, const void* h_data, uint64_t n_bytes, const uint8_t master[32],
+                  uint64_t seed_capacity, uint64_t* h_out, int device);
+int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings, uint64_t stride_bytes,
+                        uint64_t n_bytes, const uint8_t master[32], uint64_t seed_capacity, uint64_t* h_out,
+                        int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALFTIME_B200_H */

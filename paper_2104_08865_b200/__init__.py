@@ -1,0 +1,43 @@
+"""paper_2104_08865_b200 -- B200-native HalftimeHash engine.
+
+A drop-in for the hash path of the reference package ``halftimehash`` 0.1.0
+(arXiv 2104.08865): same public names as ``halftimehash/__init__.py:9-37``,
+with ``hash_bytes(..., engine="cuda")`` and the batched device entry points
+``hash_fixed`` / ``hash_varlen`` (the GPU form of ``_hash_words_np``).
+All hashing runs in hand-written sm_100a CUDA kernels in
+``libhalftime_b200.so`` (C-ABI: include/halftime_b200.h); there is no CPU
+fallback.
+"""
+
+from ._errors import SeedSizeError
+from .hasher import (
+    Digest,
+    SeedBuffer,
+    SeedLayout,
+    digest,
+    expand_seed,
+    hash_bytes,
+    instance_count,
+    seed_for_input,
+    seed_layout,
+    seed_words_needed,
+)
+from .params import VARIANTS, ErasureCode, HashParams, TransformMatrix, variant
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Digest", "ErasureCode", "HashParams", "SeedBuffer", "SeedLayout", "SeedSizeError", "TransformMatrix",
+    "VARIANTS", "digest", "expand_seed", "hash_bytes", "instance_count", "seed_for_input", "seed_layout",
+    "seed_words_needed", "variant", "hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes",
+    "__version__",
+]
+
+
+def __getattr__(name):
+    # batch entry points import torch lazily so host-only use stays light
+    if name in ("hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes"):
+        from . import batch
+
+        return getattr(batch, name)
+    raise AttributeError(name)

@@ -1,0 +1,518 @@
+// libhalftime_b200.so: C-ABI of the B200-native HalftimeHash engine.
+// Declarations and error conventions: include/halftime_b200.h.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/halftime_b200.h"
+#include "hash_kernel.cuh"
+
+using namespace hth;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? HTH_ENOMEM : HTH_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+#define CK(call)                                      \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+u64 align_up(u64 x, u64 a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  u64 n_inst, levels, ew, tree_start, tree_per, fin_start, fin_per, rem_start, rem_words, total;
+};
+// seed_layout (hasher.py:126-153)
+Layout make_layout(const VarInfo& v, u64 n_bytes) {
+  Layout l;
+  l.n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
+  l.levels = l.n_inst ? level_count(l.n_inst) : 1;
+  l.ew = (u64)v.ew;
+  l.tree_start = l.ew;
+  l.tree_per = 7 * l.levels;
+  l.fin_start = l.tree_start + l.tree_per * v.k;
+  l.fin_per = 64 * l.levels;
+  l.rem_start = l.fin_start + l.fin_per * v.k;
+  l.rem_words = (u64)v.m + v.k - 1;
+  l.total = l.rem_start + l.rem_words;
+  return l;
+}
+
+int get_var(int out, VarInfo* v) {
+  if (!var_info(out, v)) return fail(HTH_EINVAL, "unsupported output width %d; choose one of 16, 24, 32, 40", out);
+  return HTH_OK;
+}
+
+// ------------------------------------------------------------ kernels (aux)
+__device__ __forceinline__ u64 mix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void expand_seed_kernel(u64 fold, u64 start, u64 count, u64* out) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < count; i += (u64)gridDim.x * blockDim.x)
+    out[i] = mix64(fold + (start + i + 1) * 0x9E3779B97F4A7C15ull);
+}
+
+__global__ void fill_kernel(u64 seed, u64 woff, u64 n_words, u64 n_bytes, u64* dst) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_words; i += (u64)gridDim.x * blockDim.x) {
+    u64 v = mix64(seed + (woff + i + 1) * 0x9E3779B97F4A7C15ull);
+    if (i * 8 + 8 > n_bytes) {  // partial last word: write only its bytes
+      uint8_t* b = reinterpret_cast<uint8_t*>(dst + i);
+      for (u64 t = 0; i * 8 + t < n_bytes; t++) b[t] = (uint8_t)(v >> (8 * t));
+    } else {
+      dst[i] = v;
+    }
+  }
+}
+
+struct Tri {
+  u64 a, b, c;
+};
+struct TriSum {
+  __host__ __device__ Tri operator()(const Tri& x, const Tri& y) const { return {x.a + y.a, x.b + y.b, x.c + y.c}; }
+};
+
+template <int OUT>
+__global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, Tri* tri, u64* out, int* err) {
+  constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m;
+  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s <= n; s += (u64)gridDim.x * blockDim.x) {
+    if (s == n) {
+      tri[n] = {0, 0, 0};
+      continue;
+    }
+    u64 nb = off[s + 1] - off[s];
+    if (nb > max_n) {
+      atomicOr(err, 1);
+      nb = max_n;
+    }
+    const u64 ni = ((nb + 7) >> 3) / M;
+    const u64 J = ni > (u64)JOB_INST ? ceil_div(ni, JOB_INST) : 1;
+    u64 w, c;
+    scratch_need(ni, K, &w, &c);
+    tri[s] = {J, w, c};
+    if (J > 1)
+      for (int r = 0; r < K; r++) out[s * K + r] = 0;
+  }
+}
+
+__global__ void plan_fill_kernel(const Tri* meta, u64 n, u32* job_str) {
+  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < n; s += (u64)gridDim.x * blockDim.x) {
+    const u64 j0 = meta[s].a, J = meta[s + 1].a - j0;
+    for (u64 q = 0; q < J; q++) job_str[j0 + q] = (u32)s;
+  }
+}
+
+// ------------------------------------------------------------ launch config
+template <int OUT> struct KCfg;
+template <> struct KCfg<16> { static constexpr int W = 4, NS = 4; };
+template <> struct KCfg<24> { static constexpr int W = 4, NS = 3; };
+template <> struct KCfg<32> { static constexpr int W = 4, NS = 3; };
+template <> struct KCfg<40> { static constexpr int W = 4, NS = 4; };
+
+template <int OUT>
+constexpr size_t smem_bytes() {
+  constexpr int M = Geo<Var<OUT>>::m;
+  constexpr size_t SB = ROUND_INST * M * 8 + 128;
+  return KCfg<OUT>::W * KCfg<OUT>::NS * (SB + 8);
+}
+
+int sm_count(int dev) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev];
+}
+
+template <int OUT, bool VARLEN>
+int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
+  constexpr int W = KCfg<OUT>::W, NS = KCfg<OUT>::NS;
+  auto kern = hash_kernel<OUT, VARLEN, W, NS>;
+  const size_t smem = smem_bytes<OUT>();
+  static std::once_flag once[64];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  static int occ[64] = {0};
+  std::call_once(once[dev & 63], [&]() {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, W * 32, smem);
+    occ[dev & 63] = o > 0 ? o : 1;
+  });
+  u64 grid = (u64)sm_count(dev) * occ[dev & 63];
+  const u64 need = ceil_div(n_jobs_bound, W);
+  if (need < grid) grid = need;
+  if (grid == 0) grid = 1;
+  kern<<<(unsigned)grid, W * 32, smem, st>>>(P);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+
+template <bool VARLEN>
+int dispatch(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
+  switch (out) {
+    case 16: return launch_hash<16, VARLEN>(P, n_jobs_bound, st);
+    case 24: return launch_hash<24, VARLEN>(P, n_jobs_bound, st);
+    case 32: return launch_hash<32, VARLEN>(P, n_jobs_bound, st);
+    case 40: return launch_hash<40, VARLEN>(P, n_jobs_bound, st);
+  }
+  return fail(HTH_EINVAL, "unsupported output width %d", out);
+}
+
+int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
+  const Layout l = make_layout(v, n_bytes);
+  if (cap < l.total)
+    return fail(HTH_ESEEDSIZE,
+                "seed buffer holds %llu words but this input needs %llu; expand with seed_words_needed()",
+                (unsigned long long)cap, (unsigned long long)l.total);
+  return HTH_OK;
+}
+
+// fixed-mode geometry
+struct FixedPlan {
+  u64 n_inst, J, n_jobs, scr_per, cnt_per, ws_scratch, ws_cnt, ws_total;
+};
+FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
+  FixedPlan f;
+  f.n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
+  f.J = f.n_inst > (u64)JOB_INST ? ceil_div(f.n_inst, JOB_INST) : 1;
+  f.n_jobs = n_strings * f.J;
+  scratch_need(f.n_inst, v.k, &f.scr_per, &f.cnt_per);
+  f.ws_scratch = align_up(n_strings * f.scr_per * 8, 256);
+  f.ws_cnt = align_up(n_strings * f.cnt_per * 4, 256);
+  f.ws_total = f.ws_scratch + f.ws_cnt;
+  return f;
+}
+
+// varlen workspace geometry
+struct VarPlan {
+  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_cub, cub_bytes, total, max_jobs, scr_words, cnts;
+};
+int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
+  const u64 total_inst = total_bytes / (8ull * v.m);
+  p->max_jobs = n + total_inst / JOB_INST + 1;
+  p->scr_words = (total_inst / 56 + 1) * 8ull * v.k;
+  p->cnts = total_inst / 448 + 1;
+  size_t cub_bytes = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveScan(nullptr, cub_bytes, (Tri*)nullptr, (Tri*)nullptr, TriSum(),
+                                                 Tri{0, 0, 0}, (int64_t)(n + 1), (cudaStream_t)0);
+  if (e != cudaSuccess) return cuda_fail(e, "cub scan sizing");
+  p->cub_bytes = cub_bytes;
+  u64 o = 0;
+  p->off_err = o; o += 256;
+  p->off_tri = o; o = align_up(o + (n + 1) * sizeof(Tri), 256);
+  p->off_meta = o; o = align_up(o + (n + 1) * sizeof(Tri), 256);
+  p->off_jobs = o; o = align_up(o + p->max_jobs * 4, 256);
+  p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
+  p->off_cnt = o; o = align_up(o + p->cnts * 4, 256);
+  p->off_cub = o; o = align_up(o + cub_bytes, 256);
+  p->total = o;
+  return HTH_OK;
+}
+
+// per-thread e2e context (device buffers reused across calls)
+struct HostCtx {
+  int dev = -1;
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+  void* buf[3] = {nullptr, nullptr, nullptr};
+  u64 buf_bytes = 0;
+  u64* seeds = nullptr;
+  u64 seed_words = 0;
+  u64* out = nullptr;
+  u64 out_words = 0;
+  void* ws[3] = {nullptr, nullptr, nullptr};
+  u64 ws_bytes = 0;
+  ~HostCtx() {}
+};
+thread_local HostCtx g_host;
+
+int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_bytes, HostCtx** out) {
+  HostCtx& c = g_host;
+  CK(cudaSetDevice(device));
+  if (c.dev != device) {
+    c = HostCtx();
+    c.dev = device;
+    for (int i = 0; i < 3; i++) CK(cudaStreamCreateWithFlags(&c.st[i], cudaStreamNonBlocking));
+  }
+  if (buf_bytes > c.buf_bytes) {
+    for (int i = 0; i < 3; i++) {
+      if (c.buf[i]) cudaFree(c.buf[i]);
+      CK(cudaMalloc(&c.buf[i], buf_bytes));
+    }
+    c.buf_bytes = buf_bytes;
+  }
+  if (seed_words > c.seed_words) {
+    if (c.seeds) cudaFree(c.seeds);
+    CK(cudaMalloc(&c.seeds, seed_words * 8));
+    c.seed_words = seed_words;
+  }
+  if (out_words > c.out_words) {
+    if (c.out) cudaFree(c.out);
+    CK(cudaMalloc(&c.out, out_words * 8));
+    c.out_words = out_words;
+  }
+  if (ws_bytes > c.ws_bytes) {
+    for (int i = 0; i < 3; i++) {
+      if (c.ws[i]) cudaFree(c.ws[i]);
+      CK(cudaMalloc(&c.ws[i], ws_bytes));
+    }
+    c.ws_bytes = ws_bytes;
+  }
+  *out = &c;
+  return HTH_OK;
+}
+
+u64 fold_of(const uint8_t* m) {
+  u64 w[4];
+  memcpy(w, m, 32);
+  return w[0] ^ w[1] ^ w[2] ^ w[3];
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* hth_last_error(void) { return g_err.c_str(); }
+
+int hth_version(void) { return 100; }
+
+int hth_variant_geometry(int output_bytes, int* k, int* e, int* d, int* w, int* instance_words) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (k) *k = v.k;
+  if (e) *e = v.e;
+  if (d) *d = v.d;
+  if (w) *w = v.w;
+  if (instance_words) *instance_words = v.m;
+  return HTH_OK;
+}
+
+int hth_seed_words_needed(int output_bytes, uint64_t n_bytes, uint64_t* out_words) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (!out_words) return fail(HTH_EINVAL, "null output pointer");
+  *out_words = make_layout(v, n_bytes).total;
+  return HTH_OK;
+}
+
+int hth_seed_layout(int output_bytes, uint64_t n_bytes, uint64_t out10[10]) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (!out10) return fail(HTH_EINVAL, "null output pointer");
+  const Layout l = make_layout(v, n_bytes);
+  const u64 vals[10] = {l.levels, 0, l.ew, l.tree_start, l.tree_per, l.fin_start, l.fin_per, l.rem_start,
+                        l.rem_words, l.total};
+  memcpy(out10, vals, sizeof vals);
+  return HTH_OK;
+}
+
+int hth_master_fold(const uint8_t master[32], uint64_t* fold) {
+  if (!master || !fold) return fail(HTH_EINVAL, "master seed must be exactly 32 bytes");
+  *fold = fold_of(master);
+  return HTH_OK;
+}
+
+int hth_expand_seed(uint64_t fold, uint64_t start, uint64_t count, uint64_t* d_words, void* stream) {
+  if (!count) return HTH_OK;
+  if (!d_words) return fail(HTH_EINVAL, "null seed buffer");
+  const u64 blocks = std::min<u64>(ceil_div(count, 256), 4096);
+  expand_seed_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(fold, start, count, d_words);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+
+int hth_fill_splitmix(uint64_t fill_seed, uint64_t word_offset, uint64_t n_bytes, void* d_dst, void* stream) {
+  if (!n_bytes) return HTH_OK;
+  if (!d_dst || (reinterpret_cast<uintptr_t>(d_dst) & 7)) return fail(HTH_EINVAL, "destination must be 8-byte aligned");
+  const u64 nw = (n_bytes + 7) / 8;
+  const u64 blocks = std::min<u64>(ceil_div(nw, 256), 148 * 64);
+  fill_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(fill_seed, word_offset, nw, n_bytes, (u64*)d_dst);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+
+int hth_workspace_size_fixed(int output_bytes, uint64_t n_strings, uint64_t n_bytes, uint64_t* bytes) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (!bytes) return fail(HTH_EINVAL, "null output pointer");
+  *bytes = fixed_plan(v, n_strings, n_bytes).ws_total;
+  return HTH_OK;
+}
+
+int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uint64_t stride_bytes, uint64_t n_bytes,
+                   const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out, void* d_workspace,
+                   uint64_t workspace_bytes, void* stream) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
+  if (!n_strings) return HTH_OK;
+  if (!d_out || !d_seed) return fail(HTH_EINVAL, "null device pointer");
+  if (n_bytes && !d_data) return fail(HTH_EINVAL, "null data pointer");
+  if (reinterpret_cast<uintptr_t>(d_data) & 15) return fail(HTH_EINVAL, "d_data must be 16-byte aligned");
+  if (n_strings > 1 && stride_bytes < n_bytes) return fail(HTH_EINVAL, "stride_bytes < n_bytes");
+  const FixedPlan f = fixed_plan(v, n_strings, n_bytes);
+  if (workspace_bytes < f.ws_total)
+    return fail(HTH_EINVAL, "workspace too small: %llu < %llu bytes", (unsigned long long)workspace_bytes,
+                (unsigned long long)f.ws_total);
+  cudaStream_t st = (cudaStream_t)stream;
+  Params P{};
+  P.data = (const uint8_t*)d_data;
+  P.n_strings = n_strings;
+  P.stride = stride_bytes;
+  P.n_bytes = n_bytes;
+  P.J_fixed = f.J;
+  P.n_jobs = f.n_jobs;
+  P.scr_per = f.scr_per;
+  P.cnt_per = f.cnt_per;
+  P.S = d_seed;
+  P.out = d_out;
+  P.scratch = (u64*)d_workspace;
+  P.counters = (u32*)((uint8_t*)d_workspace + f.ws_scratch);
+  if (f.J > 1) CK(cudaMemsetAsync(d_out, 0, n_strings * v.k * 8, st));
+  if (f.cnt_per) CK(cudaMemsetAsync(P.counters, 0, n_strings * f.cnt_per * 4, st));
+  return dispatch<false>(output_bytes, P, f.n_jobs, st);
+}
+
+int hth_workspace_size_varlen(int output_bytes, uint64_t n_strings, uint64_t total_bytes, uint64_t* bytes) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (!bytes) return fail(HTH_EINVAL, "null output pointer");
+  VarPlan p;
+  if (int rc = varlen_plan(v, n_strings, total_bytes, &p)) return rc;
+  *bytes = p.total;
+  return HTH_OK;
+}
+
+int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offsets, uint64_t n_strings,
+                    uint64_t max_n_bytes, uint64_t total_bytes, const uint64_t* d_seed, uint64_t seed_capacity,
+                    uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (int rc = check_seed(v, max_n_bytes, seed_capacity)) return rc;
+  if (!n_strings) return HTH_OK;
+  if (!d_out || !d_seed || !d_offsets || !d_workspace) return fail(HTH_EINVAL, "null device pointer");
+  if (reinterpret_cast<uintptr_t>(d_data) & 15) return fail(HTH_EINVAL, "d_data must be 16-byte aligned");
+  if (n_strings >= (1ull << 32)) return fail(HTH_EINVAL, "at most 2^32-1 strings per call");
+  VarPlan p;
+  if (int rc = varlen_plan(v, n_strings, total_bytes, &p)) return rc;
+  if (workspace_bytes < p.total)
+    return fail(HTH_EINVAL, "workspace too small: %llu < %llu bytes", (unsigned long long)workspace_bytes,
+                (unsigned long long)p.total);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)d_workspace;
+  int* err = (int*)(ws + p.off_err);
+  Tri* tri = (Tri*)(ws + p.off_tri);
+  Tri* meta = (Tri*)(ws + p.off_meta);
+  u32* jobs = (u32*)(ws + p.off_jobs);
+  CK(cudaMemsetAsync(err, 0, 4, st));
+  CK(cudaMemsetAsync(ws + p.off_cnt, 0, p.cnts * 4, st));
+  const u64 blocks = std::min<u64>(ceil_div(n_strings + 1, 256), 4096);
+  switch (output_bytes) {
+    case 16: plan_count_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
+    case 24: plan_count_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
+    case 32: plan_count_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
+    case 40: plan_count_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
+  }
+  CK(cudaGetLastError());
+  size_t cub_bytes = p.cub_bytes;
+  CK(cub::DeviceScan::ExclusiveScan(ws + p.off_cub, cub_bytes, tri, meta, TriSum(), Tri{0, 0, 0},
+                                    (int64_t)(n_strings + 1), st));
+  plan_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(meta, n_strings, jobs);
+  CK(cudaGetLastError());
+  Params P{};
+  P.data = (const uint8_t*)d_data;
+  P.n_strings = n_strings;
+  P.offsets = d_offsets;
+  P.job_str = jobs;
+  P.meta = (const u64*)meta;
+  P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_count)
+  P.S = d_seed;
+  P.out = d_out;
+  P.scratch = (u64*)(ws + p.off_scr);
+  P.counters = (u32*)(ws + p.off_cnt);
+  return dispatch<true>(output_bytes, P, p.max_jobs, st);
+}
+
+int hth_varlen_status(void* d_workspace, void* stream) {
+  if (!d_workspace) return fail(HTH_EINVAL, "null workspace");
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, d_workspace, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  if (h) return fail(HTH_ESEEDSIZE, "a string was longer than max_n_bytes; its digest is invalid");
+  return HTH_OK;
+}
+
+int hth_hash_host(int output_bytes, const void* h_data, uint64_t n_bytes, const uint8_t master[32],
+                  uint64_t seed_capacity, uint64_t* h_out, int device) {
+  return hth_hash_fixed_host(output_bytes, h_data, 1, n_bytes, n_bytes, master, seed_capacity, h_out, device);
+}
+
+int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings, uint64_t stride_bytes,
+                        uint64_t n_bytes, const uint8_t master[32], uint64_t seed_capacity, uint64_t* h_out,
+                        int device) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (!master) return fail(HTH_EINVAL, "master seed must be exactly 32 bytes");
+  const Layout lay = make_layout(v, n_bytes);
+  if (seed_capacity && seed_capacity < lay.total) return check_seed(v, n_bytes, seed_capacity);
+  if (!n_strings) return HTH_OK;
+  if (!h_out || (n_bytes && !h_data)) return fail(HTH_EINVAL, "null host pointer");
+  if (n_strings > 1 && stride_bytes < n_bytes) return fail(HTH_EINVAL, "stride_bytes < n_bytes");
+  if (n_strings == 1) stride_bytes = align_up(n_bytes, 16);
+  // chunking: whole strings per chunk, ~64 MiB per chunk, 3 buffers in flight
+  const u64 target = 64ull << 20;
+  // strings keep their host stride on the device (the kernel handles any
+  // start alignment); only the chunk base is 16-byte aligned
+  const u64 dstride = std::max<u64>(stride_bytes, 1);
+  u64 per = std::max<u64>(1, target / dstride);
+  if (per > n_strings) per = n_strings;
+  const u64 nchunks = ceil_div(n_strings, per);
+  const FixedPlan fp = fixed_plan(v, per, n_bytes);
+  HostCtx* c = nullptr;
+  if (int rc = host_ctx(device, per * dstride + 16, lay.total, n_strings * v.k, std::max<u64>(fp.ws_total, 256), &c))
+    return rc;
+  if (int rc = hth_expand_seed(fold_of(master), 0, lay.total, c->seeds, c->st[0])) return rc;
+  cudaEvent_t seeded;
+  CK(cudaEventCreateWithFlags(&seeded, cudaEventDisableTiming));
+  CK(cudaEventRecord(seeded, c->st[0]));
+  for (int i = 1; i < 3; i++) CK(cudaStreamWaitEvent(c->st[i], seeded, 0));
+  for (u64 ch = 0; ch < nchunks; ch++) {
+    const int b = (int)(ch % 3);
+    cudaStream_t st = c->st[b];
+    const u64 s0 = ch * per, ns = std::min(per, n_strings - s0);
+    const uint8_t* src = (const uint8_t*)h_data + s0 * stride_bytes;
+    if (n_bytes) CK(cudaMemcpyAsync(c->buf[b], src, (ns - 1) * stride_bytes + n_bytes, cudaMemcpyHostToDevice, st));
+    if (int rc = hth_hash_fixed(output_bytes, c->buf[b], ns, dstride, n_bytes, c->seeds, lay.total,
+                                c->out + s0 * v.k, c->ws[b], c->ws_bytes, st))
+      return rc;
+    CK(cudaMemcpyAsync(h_out + s0 * v.k, c->out + s0 * v.k, ns * v.k * 8, cudaMemcpyDeviceToHost, st));
+  }
+  for (int i = 0; i < 3; i++) CK(cudaStreamSynchronize(c->st[i]));
+  cudaEventDestroy(seeded);
+  return HTH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+"""Drop-in mirror of the reference's public hash API
+(halftimehash/hasher.py:36-176, 434-461), served by the CUDA engine.
+
+``hash_bytes(data, seed, params, engine="cuda")`` and ``digest`` keep the
+reference's names, argument meaning and errors:
+
+* ``ValueError``    unsupported width (params.py:230-237), bad master
+                    (hasher.py:48-50), unknown engine / counter with a
+                    non-scalar engine (hasher.py:447-453)
+* ``SeedSizeError`` capacity below ``seed_words_needed`` (hasher.py:209-214)
+* ``IndexError``    seed word out of range (hasher.py:84-97)
+
+The only engine is ``"cuda"``: the reference's ``"lanes"`` and ``"scalar"``
+are CPU engines and are deliberately not present (no CPU fallback).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._errors import SeedSizeError
+from .params import HashParams, variant
+
+GOLDEN_GAMMA = 0x9E3779B97F4A7C15
+_MIX_1 = 0xBF58476D1CE4E5B9
+_MIX_2 = 0x94D049BB133111EB
+MASK64 = (1 << 64) - 1
+
+__all__ = [
+    "Digest", "SeedBuffer", "SeedLayout", "SeedSizeError", "digest", "expand_seed", "hash_bytes",
+    "seed_for_input", "seed_layout", "seed_words_needed", "instance_count", "splitmix_mix",
+]
+
+
+def splitmix_mix(z: int) -> int:
+    """splitmix64 finalizer (hasher.py:40-45)."""
+    z &= MASK64
+    z = ((z ^ (z >> 30)) * _MIX_1) & MASK64
+    z = ((z ^ (z >> 27)) * _MIX_2) & MASK64
+    return z ^ (z >> 31)
+
+
+def _master_fold(master: bytes) -> int:
+    if not isinstance(master, (bytes, bytearray)) or len(master) != 32:
+        raise ValueError("master seed must be exactly 32 bytes")
+    a, b, c, d = struct.unpack("<4Q", bytes(master))
+    return a ^ b ^ c ^ d
+
+
+def _stream_words_np(fold, start: int, count: int) -> np.ndarray:
+    idx = np.arange(start + 1, start + count + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.asarray(fold, dtype=np.uint64) + idx * np.uint64(GOLDEN_GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(_MIX_1)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(_MIX_2)
+    return z ^ (z >> np.uint64(31))
+
+
+@dataclass(frozen=True)
+class SeedBuffer:
+    """Deterministic expansion of a 32-byte master seed (hasher.py:70-97).
+
+    Host accessors (``word``, ``words``, ``words_np``) keep the reference's
+    semantics; ``device_words`` materialises S[0..capacity) on a GPU with the
+    ``hth_expand_seed`` kernel and caches it per device.
+    """
+
+    master: bytes
+    capacity: int
+    fold: int
+    _dev: dict = field(default_factory=dict, compare=False, repr=False, hash=False)
+
+    @classmethod
+    def from_master(cls, master: bytes, capacity: int) -> "SeedBuffer":
+        if capacity < 0:
+            raise ValueError("capacity must be nonnegative")
+        return cls(bytes(master), capacity, _master_fold(master))
+
+    def word(self, index: int) -> int:
+        if not 0 <= index < self.capacity:
+            raise IndexError("seed word index out of range")
+        return splitmix_mix((self.fold + (index + 1) * GOLDEN_GAMMA) & MASK64)
+
+    def words(self, start: int, count: int) -> list:
+        if start < 0 or start + count > self.capacity:
+            raise IndexError("seed word range out of range")
+        return [int(x) for x in _stream_words_np(self.fold, start, count)]
+
+    def words_np(self, start: int, count: int) -> np.ndarray:
+        if start < 0 or start + count > self.capacity:
+            raise IndexError("seed word range out of range")
+        return _stream_words_np(self.fold, start, count)
+
+    def device_words(self, device=None):
+        """S[0..capacity) as a CUDA int64 tensor (raw u64 bits), cached per device."""
+        import torch
+
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+        t = self._dev.get(dev.index)
+        if t is None:
+            t = torch.empty(max(self.capacity, 1), dtype=torch.int64, device=dev)
+            with torch.cuda.device(dev):
+                st = torch.cuda.current_stream(dev).cuda_stream
+                _lib.check(_lib.lib().hth_expand_seed(self.fold, 0, self.capacity, t.data_ptr(), st))
+            self._dev[dev.index] = t
+        return t
+
+
+def expand_seed(master: bytes, needed: int) -> SeedBuffer:
+    """Expand a 32-byte master into ``needed`` words (hasher.py:100-102)."""
+    return SeedBuffer.from_master(master, needed)
+
+
+@dataclass(frozen=True)
+class SeedLayout:
+    """Region partition of the expanded words for one length (hasher.py:105-123)."""
+
+    levels: int
+    ehc_start: int
+    ehc_words: int
+    tree_start: int
+    tree_words_per_tree: int
+    finalize_start: int
+    finalize_words_per_tree: int
+    remainder_start: int
+    remainder_words: int
+    total_words: int
+
+
+def _check_params(params: HashParams) -> HashParams:
+    if not isinstance(params, HashParams):
+        raise ValueError("params must be a HashParams from variant()")
+    return params
+
+
+def instance_count(params: HashParams, n_bytes: int) -> int:
+    return ((n_bytes + 7) // 8) // params.instance_words
+
+
+def seed_layout(params: HashParams, n_bytes: int) -> SeedLayout:
+    """Served by the C-ABI (hth_seed_layout) so host and device share one formula."""
+    out = (ctypes.c_uint64 * 10)()
+    _lib.check(_lib.lib().hth_seed_layout(_check_params(params).output_bytes, n_bytes, out))
+    return SeedLayout(*[int(x) for x in out])
+
+
+def seed_words_needed(params: HashParams, n_bytes: int) -> int:
+    """Seed words needed to hash ``n_bytes`` (hasher.py:156-158)."""
+    out = _lib.u64_out()
+    _lib.check(_lib.lib().hth_seed_words_needed(_check_params(params).output_bytes, n_bytes, ctypes.byref(out)))
+    return int(out.value)
+
+
+def seed_for_input(master: bytes, params: HashParams, n_bytes: int) -> SeedBuffer:
+    return expand_seed(master, seed_words_needed(params, n_bytes))
+
+
+@dataclass(frozen=True)
+class Digest:
+    """k little-endian 64-bit words; ``output_bytes = 8 * k`` (hasher.py:165-176)."""
+
+    words: tuple
+
+    @property
+    def bytes(self) -> bytes:
+        return b"".join(w.to_bytes(8, "little") for w in self.words)
+
+    def hex(self) -> str:
+        return self.bytes.hex()
+
+
+def _check_capacity(seed: SeedBuffer, params: HashParams, n_bytes: int) -> None:
+    need = seed_words_needed(params, n_bytes)
+    if seed.capacity < need:
+        raise SeedSizeError(
+            f"seed buffer holds {seed.capacity} words but this input needs {need}; "
+            "expand with seed_words_needed()")
+
+
+def hash_bytes(data, seed: SeedBuffer, params: HashParams, engine: str = "cuda", counter=None,
+               device=None) -> Digest:
+    """One-shot hash of ``data`` under an expanded seed (hasher.py:434-453).
+
+    ``data`` is a bytes-like object (host) or a CUDA uint8 tensor (device).
+    Host data goes through ``hth_hash_host`` (H2D copy, on-device seed
+    expansion, hash, D2H); device data through ``hth_hash_fixed``.
+    """
+    if engine != "cuda":
+        raise ValueError(f"unknown engine {engine!r} (this package provides engine='cuda' only)")
+    if counter is not None:
+        raise ValueError("multiplication counting requires engine='scalar'")
+    params = _check_params(params)
+    k = params.output_words
+    try:
+        import torch
+        is_tensor = isinstance(data, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_tensor = False
+    if is_tensor:
+        from .batch import hash_fixed
+
+        n = data.numel()
+        _check_capacity(seed, params, n)
+        out = hash_fixed(data.reshape(1, n), n, seed, params)
+        return Digest(tuple(int(x) for x in out.cpu().numpy().view(np.uint64)[0]))
+    buf = bytes(data)
+    _check_capacity(seed, params, len(buf))
+    out = (ctypes.c_uint64 * k)()
+    dev = 0 if device is None else int(device)
+    _lib.check(_lib.lib().hth_hash_host(params.output_bytes, buf, len(buf), seed.master, seed.capacity,
+                                        out, dev))
+    return Digest(tuple(int(x) for x in out))
+
+
+def digest(data, master: bytes = b"\x00" * 32, output_bytes: int = 24) -> Digest:
+    """Convenience one-shot (hasher.py:456-461)."""
+    params = variant(output_bytes)
+    return hash_bytes(data, seed_for_input(master, params, len(data)), params)

@@ -1,0 +1,203 @@
+"""CUDA engine parity against the oracle and the reference's golden vectors.
+
+Every digest produced by libhalftime_b200.so must equal the reference's bit
+for bit (integer work: no tolerance)."""
+
+import numpy as np
+import pytest
+
+from oracle import c as coracle
+from oracle import oracle_np as o
+
+from _golden import classic_cases, gen_bytes, records
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = (16, 24, 32, 40)
+
+
+@pytest.fixture(scope="module")
+def hh():
+    import torch
+
+    import paper_2104_08865_b200 as h
+
+    assert torch.cuda.is_available()
+    return h
+
+
+def _hex(words):
+    return b"".join(int(x).to_bytes(8, "little") for x in words).hex()
+
+
+def _u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+# ------------------------------------------------------------------ goldens
+@pytest.mark.parametrize("case", classic_cases(), ids=lambda c: f"{c[0]}-{len(c[2])}")
+def test_reference_golden_digests(hh, case):
+    w, master, data, hexd = case
+    assert hh.digest(data, master, w).hex() == hexd
+
+
+def test_fixture_records_public_api(hh):
+    recs = [r for r in records() if r["kind"] in ("lanes", "scalar", "cli_grid", "capacity")]
+    bad = []
+    for r in recs:
+        w, n = r["variant"], r["length"]
+        p = hh.variant(w)
+        data = gen_bytes(r["generator"], n)
+        master = bytes.fromhex(r["master"])
+        cap = r.get("capacity", hh.seed_words_needed(p, n))
+        d = hh.hash_bytes(data, hh.expand_seed(master, cap), p)
+        if d.hex() != r["digest"]:
+            bad.append((w, n, r["kind"]))
+    assert not bad, bad[:20]
+
+
+def test_fixture_records_device_tensor(hh):
+    import torch
+
+    for r in records("lanes")[::7]:
+        w, n = r["variant"], r["length"]
+        p = hh.variant(w)
+        data = torch.frombuffer(bytearray(gen_bytes(r["generator"], n)) or bytearray(1), dtype=torch.uint8)[:n]
+        seed = hh.seed_for_input(bytes.fromhex(r["master"]), p, n)
+        assert hh.hash_bytes(data.cuda(), seed, p).hex() == r["digest"], (w, n)
+
+
+# ------------------------------------------------------------------ batches
+def _check_fixed(hh, w, n_strings, n_bytes, stride=None, seed_fold=3, data_seed=11):
+    import torch
+
+    p = hh.variant(w)
+    stride = n_bytes if stride is None else stride
+    total = (n_strings - 1) * stride + n_bytes if n_strings else 0
+    buf = hh.fill_bytes(total, data_seed)
+    master = seed_fold.to_bytes(8, "little") + bytes(24)
+    seed = hh.seed_for_input(master, p, n_bytes)
+    got = _u64(hh.hash_fixed(buf, n_bytes, seed, p, n_strings=n_strings, stride=stride))
+    host = np.frombuffer(o.fill_bytes(total, data_seed), dtype=np.uint8).copy() if total else np.zeros(16, np.uint8)
+    S = o.splitmix_words(seed_fold, 0, o.seed_words_needed(o.variant(w), n_bytes))
+    want = coracle.hash_fixed(w, host, n_strings, stride, n_bytes, S)
+    bad = np.nonzero(~np.all(got == want, axis=1))[0]
+    assert bad.size == 0, f"v{w} n={n_bytes} stride={stride}: {bad.size} mismatches, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("w", VARIANTS)
+def test_every_short_length(hh, w):
+    # n = 0..127 (all tail-only) plus instance/block boundaries, batch of 33
+    v = o.variant(w)
+    iw = v.m * 8
+    lengths = list(range(0, 128)) + [iw - 9, iw - 8, iw - 1, iw, iw + 1, iw + 7, iw + 8, 2 * iw - 1, 2 * iw,
+                                     2 * iw + 1, 4 * iw - 1, 4 * iw, 4 * iw + 3, 5 * iw + 100, 7 * iw + 5,
+                                     8 * iw - 1, 8 * iw, 8 * iw + 1, 9 * iw - 3]
+    for n in lengths:
+        _check_fixed(hh, w, 33, n)
+
+
+@pytest.mark.parametrize("w", VARIANTS)
+def test_multi_job_and_tree_levels(hh, w):
+    # job boundaries (64 instances), level-2 / level-3 merges, powers of 8 +- 1
+    v = o.variant(w)
+    iw = v.m * 8
+    for inst in (63, 64, 65, 127, 128, 129, 511, 512, 513, 575, 1092, 4095, 4096, 4097):
+        for extra in (0, 13):
+            _check_fixed(hh, w, 5, inst * iw + extra)
+
+
+@pytest.mark.parametrize("w", VARIANTS)
+def test_unaligned_stride(hh, w):
+    for stride_extra in (1, 3, 8, 9):
+        n = 3000 + 17 * stride_extra
+        _check_fixed(hh, w, 40, n, stride=n + stride_extra)
+
+
+@pytest.mark.parametrize("w", VARIANTS)
+def test_varlen_packed(hh, w):
+    import torch
+
+    from workloads import cfg2_lengths, offsets_of
+
+    lengths = cfg2_lengths(2048, seed=w)
+    lengths[::97] = np.arange(0, len(lengths[::97])) * 41 % 3000 + 70000  # a few multi-job strings
+    off = offsets_of(lengths)
+    total = int(off[-1])
+    buf = hh.fill_bytes(total, 5)
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, int(lengths.max()))
+    got = _u64(hh.hash_varlen(buf, off, seed, p))
+    host = np.frombuffer(o.fill_bytes(total, 5), dtype=np.uint8).copy()
+    S = seed.words_np(0, seed.capacity)
+    want = coracle.hash_varlen(w, host, off, S)
+    bad = np.nonzero(~np.all(got == want, axis=1))[0]
+    assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]} offsets {off[bad[:8]] % 16}"
+
+
+@pytest.mark.parametrize("w", (16, 40))
+def test_long_single_string(hh, w):
+    # multi-level last-arriver merges within one string (n_inst >> 8^3)
+    import torch
+
+    v = o.variant(w)
+    n = 64 * 4096 * v.m * 8 + 777  # 262,144 instances -> 6 levels
+    buf = hh.fill_bytes(n, 9)
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, n)
+    got = _u64(hh.hash_fixed(buf, n, seed, p))[0]
+    host = np.frombuffer(o.fill_bytes(n, 9), dtype=np.uint8).copy()
+    want = coracle.hash_huge(w, host, seed.words_np(0, seed.capacity))
+    assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------ API/errors
+def test_seed_size_error_and_capacity(hh):
+    p = hh.variant(24)
+    data = bytes(100000)
+    small = hh.expand_seed(b"\0" * 32, hh.seed_words_needed(p, 64))
+    with pytest.raises(hh.SeedSizeError):
+        hh.hash_bytes(data, small, p)
+    d = o.fill_bytes(5000)
+    exact = hh.hash_bytes(d, hh.seed_for_input(b"\0" * 32, p, len(d)), p)
+    big = hh.hash_bytes(d, hh.expand_seed(b"\0" * 32, 10 ** 5), p)
+    assert exact == big
+
+
+def test_engine_and_counter_errors(hh):
+    p = hh.variant(24)
+    s = hh.seed_for_input(b"\0" * 32, p, 0)
+    with pytest.raises(ValueError):
+        hh.hash_bytes(b"", s, p, engine="lanes")
+    with pytest.raises(ValueError):
+        hh.hash_bytes(b"", s, p, counter=object())
+    with pytest.raises(ValueError):
+        hh.digest(b"", b"\0" * 32, 20)
+
+
+def test_device_seed_expansion_matches_host(hh):
+    s = hh.expand_seed(bytes(range(32)), 3000)
+    dev = s.device_words().cpu().numpy().view(np.uint64)
+    assert np.array_equal(dev, s.words_np(0, 3000))
+
+
+def test_host_batch_entry(hh):
+    p = hh.variant(40)
+    n, B = 70000, 37
+    host = np.frombuffer(o.fill_bytes(B * n, 4), dtype=np.uint8).copy()
+    got = hh.hash_fixed_host(host, B, n, bytes(range(32)), p)
+    S = o.splitmix_words(o.master_fold(bytes(range(32))), 0, o.seed_words_needed(o.variant(40), n))
+    want = coracle.hash_fixed(40, host, B, n, n, S)
+    assert np.array_equal(got, want)
+
+
+def test_hash_words_seam(hh):
+    # the _hash_words_np seam (hasher.py:331-413) on a (B, n_words) batch
+    p = hh.variant(32)
+    n_bytes = 2048
+    rng = np.random.default_rng(0)
+    words = rng.integers(0, 1 << 64, size=(100, n_bytes // 8), dtype=np.uint64)
+    seed = hh.seed_for_input(bytes(range(32)), p, n_bytes)
+    got = hh.hash_words(words, n_bytes, seed, p)
+    want = o.hash_batch(o.variant(32), words, n_bytes, seed.words_np(0, seed.capacity))
+    assert np.array_equal(got, want)
