@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""HalftimeHash B200 benchmark (driver contract: one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload cfg4] [--no-extra] [--e2e-steps E]
+
+Headline workload: config 4 of BASELINE.json -- 8192 strings x 1 MiB per GPU
+(8 GiB, 40-byte variant), the largest batch config and the one quoted per GPU
+and per box; strings are sharded round-robin across ranks (weak scaling, no
+data-path collective).  A "step" is one pass of the hash over the whole
+batch: exactly one hash_kernel launch.  Inputs (8 GiB) exceed L2 (126 MB),
+so no flush is needed between steps.  At N=1 rank 0 also measures the other
+configs (cfg1, cfg2, cfg3, cfg5) into "workloads" (cfg1/cfg2 with an L2
+flush between timed iterations).
+
+--impl reference times the reference's CPU algorithm (the numpy restatement
+oracle/oracle_np.py of halftimehash's lane engine, hasher.py:331-413; the
+reference itself is Python and cannot travel to the GPU box) on all host
+cores over a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as wl  # noqa: E402
+
+METRIC = "GB/s hashed"
+UNIT = "GB/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic(workload):
+    """dram read+write bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(workload)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0=None, t1=None):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = [l for (t, l) in self.lines if (t0 is None or t >= t0 - 0.06) and (t1 is None or t <= t1 + 0.06)]
+        if not rows:
+            rows = [l for (_, l) in self.lines]
+        for l in rows:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU side
+def _cpu_worker(args):
+    """Hash `count` strings of a fixed-length config with the numpy oracle; returns bytes hashed."""
+    w, n_bytes, first, count, stride = args
+    from oracle import oracle_np as o
+
+    v = o.variant(w)
+    S = o.splitmix_words(o.master_fold(wl.MASTER), 0, o.seed_words_needed(v, n_bytes))
+    done = 0
+    for s in range(first, first + count):
+        data = wl.host_bytes(s * stride, n_bytes)
+        words = o.words_from_bytes(data)[None, :]
+        o.hash_batch(v, words, n_bytes, S)
+        done += n_bytes
+    return done
+
+
+def cpu_rate(workload: str, per_core: int, cores: int):
+    """Reference CPU algorithm on `cores` processes, `per_core` strings each (bounded sample)."""
+    cfg = wl.CONFIGS[workload]
+    w, n = cfg["variant"], cfg["n_bytes"]
+    if workload == "cfg5":  # one huge string: sample f^c-aligned instance chunks of it
+        n = 16 << 20
+    jobs = [(w, n, i * per_core, per_core, n) for i in range(cores)]
+    t0 = time.perf_counter()
+    if cores == 1:
+        total = sum(_cpu_worker(j) for j in jobs)
+    else:
+        with mp.get_context("fork").Pool(cores) as pool:
+            total = sum(pool.map(_cpu_worker, jobs))
+    dt = time.perf_counter() - t0
+    return total / dt / 1e9, total, dt
+
+
+# ---------------------------------------------------------------- GPU side
+def _algo_bytes(workload, n_strings, n_bytes, k):
+    return n_strings * n_bytes + n_strings * k * 8
+
+
+def setup_fixed(hh, torch, workload, rank=0, world=1):
+    cfg = wl.CONFIGS[workload]
+    w, n = cfg["variant"], cfg["n_bytes"]
+    B = cfg["n_strings"]
+    p = hh.variant(w)
+    buf = torch.empty(B * n + 64, dtype=torch.uint8, device="cuda")
+    if world == 1:
+        hh.fill_bytes(B * n, wl.DATA_SEED, 0, out=buf)
+    else:  # round-robin: local string i is global string rank + i * world
+        for i in range(B):
+            g = rank + i * world
+            hh.fill_bytes(n, wl.DATA_SEED, g * n // 8, out=buf[i * n:(i + 1) * n + 16])
+    seed = hh.seed_for_input(wl.MASTER, p, n)
+    st = seed.device_words()
+    out = torch.empty((B, p.output_words), dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    return dict(p=p, buf=buf, seed=seed, out=out, B=B, n=n, w=w)
+
+
+def run_fixed(hh, torch, ctx, steps, warmup, flush=None):
+    p, buf, seed, out, B, n = ctx["p"], ctx["buf"], ctx["seed"], ctx["out"], ctx["B"], ctx["n"]
+    stream = torch.cuda.current_stream()
+
+    def step():
+        hh.hash_fixed(buf, n, seed, p, n_strings=B, stride=n, out=out)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    t_start.record(stream)
+    for i in range(steps):
+        if flush is not None:
+            flush()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    wall1 = time.time()
+    per = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(per) if flush is not None else t_start.elapsed_time(t_end)
+    return total_ms, per, (wall0, wall1)
+
+
+def make_flush(torch):
+    big = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def flush():
+        big.fill_(1)
+
+    return flush
+
+
+def measure_workload(hh, torch, workload, steps, warmup, peak):
+    """N=1 secondary measurement of one config (rank 0 only)."""
+    res = {"desc": wl.CONFIGS[workload]["desc"]}
+    if workload == "cfg2":
+        lengths = wl.cfg2_lengths()
+        off = wl.offsets_of(lengths)
+        total = int(off[-1])
+        buf = torch.empty(total + 64, dtype=torch.uint8, device="cuda")
+        hh.fill_bytes(total, wl.DATA_SEED, 0, out=buf)
+        d_off = torch.from_numpy(off.view(np.int64)).cuda()
+        mx = int(lengths.max())
+        seeds = {w: hh.seed_for_input(wl.MASTER, hh.variant(w), mx) for w in (16, 24, 32, 40)}
+        outs = {w: torch.empty((len(lengths), w // 8), dtype=torch.int64, device="cuda") for w in seeds}
+        for w in seeds:
+            seeds[w].device_words()
+        flush = make_flush(torch)
+
+        def step():
+            for w in (16, 24, 32, 40):
+                hh.hash_varlen(buf, d_off, seeds[w], hh.variant(w), max_n_bytes=mx, out=outs[w])
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        per = []
+        stream = torch.cuda.current_stream()
+        for _ in range(steps):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            per.append(a.elapsed_time(b))
+        ms = statistics.mean(per)
+        nbytes = 4 * total + 4 * len(lengths) * 0  # digests negligible
+        res.update(value=4 * total / (ms / 1e3) / 1e9, ms_per_step=ms, bytes_per_step=4 * total,
+                   l2="flushed (256 MB write) before every timed step", launches_per_step=4 * 5)
+        del buf
+        return res
+    ctx = setup_fixed(hh, torch, workload)
+    flush = make_flush(torch) if workload == "cfg1" else None
+    k = ctx["p"].output_words
+    total_ms, per, _ = run_fixed(hh, torch, ctx, steps, warmup, flush)
+    ms = total_ms / steps
+    algo = _algo_bytes(workload, ctx["B"], ctx["n"], k)
+    gbs = ctx["B"] * ctx["n"] / (ms / 1e3) / 1e9
+    res.update(value=gbs, ms_per_step=ms, bytes_per_step=ctx["B"] * ctx["n"],
+               roofline_frac=(algo / (ms / 1e3) / 1e9) / peak,
+               l2="flushed before every timed step" if flush else "inputs larger than L2 (126 MB)")
+    del ctx
+    torch.cuda.empty_cache()
+    return res
+
+
+def e2e_fixed(hh, torch, workload, steps, n_strings_cap=None):
+    """Public host-buffer API (hth_hash_fixed_host) from pinned memory: H2D + hash + D2H per step."""
+    cfg = wl.CONFIGS[workload]
+    w, n, B = cfg["variant"], cfg["n_bytes"], cfg["n_strings"]
+    if n_strings_cap:
+        B = min(B, n_strings_cap)
+    p = hh.variant(w)
+    dev = torch.empty(B * n + 16, dtype=torch.uint8, device="cuda")
+    hh.fill_bytes(B * n, wl.DATA_SEED, 0, out=dev)
+    host = torch.empty(B * n, dtype=torch.uint8, pin_memory=True)
+    host.copy_(dev[:B * n])
+    del dev
+    torch.cuda.empty_cache()
+    hh.hash_fixed_host(host, B, n, wl.MASTER, p)  # warm-up (allocates staging buffers)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = hh.hash_fixed_host(host, B, n, wl.MASTER, p)
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    return {"value": B * n / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": B * n,
+            "d2h_bytes_per_step": B * p.output_words * 8, "strings_per_step": B,
+            "steps": steps, "api": "hth_hash_fixed_host (pinned host memory, 3-stream chunked H2D/hash/D2H)"}, out
+
+
+# ---------------------------------------------------------------- arms
+def arm_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    workload = args.workload
+    cores = os.cpu_count() or 1
+    per_core = {"cfg1": 256, "cfg3": 1024, "cfg4": 2, "cfg5": 1, "cfg2": 64}.get(workload, 2)
+    cpu_rate(workload, 1, min(cores, 2))  # warm-up (imports, fork)
+    for _ in range(max(args.warmup - 1, 0)):
+        cpu_rate(workload, 1, min(cores, 2))
+    rates, dts, tot = [], [], 0
+    for _ in range(args.steps):
+        r, b, dt = cpu_rate(workload, per_core, cores)
+        rates.append(r)
+        dts.append(dt)
+        tot = b
+    value = statistics.median(rates)
+    cfg = wl.CONFIGS[workload]
+    sample = f"{cores} processes x {per_core} strings of {cfg.get('n_bytes')} B (v{cfg['variant']}) per step"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(dts) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (splitmix stream, seed 0)",
+        "config": {"workload": workload, "desc": cfg["desc"], "variant": cfg["variant"],
+                   "bytes_per_step": tot},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample + "; numpy restatement of hasher.py:331-413 (oracle/oracle_np.py)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def arm_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2104_08865_b200 as hh
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    peak, peak_src = _peaks()
+    workload = args.workload
+    ctx = setup_fixed(hh, torch, workload, rank, world)
+    k = ctx["p"].output_words
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms, per, (w0, w1) = run_fixed(hh, torch, ctx, args.steps, args.warmup)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    time.sleep(0.2)
+    sampler.stop()
+    clocks = sampler.summary(w0, w1)
+    kernel_ms = statistics.mean(per)  # one hash_kernel launch per step, events on its stream
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms = total_ms / args.steps
+    B, n = ctx["B"], ctx["n"]
+    value = world * B * n / (ms / 1e3) / 1e9
+    algo = _algo_bytes(workload, B, n, k)
+    achieved = algo / (kernel_ms / 1e3) / 1e9
+    # digests stay sharded; rank 0 checks a sample of its digests against the oracle
+    check = None
+    if rank == 0 and not args.no_check:
+        from oracle import c as coracle
+        from oracle import oracle_np as o
+
+        got = ctx["out"][:4].cpu().numpy().view(np.uint64)
+        host = np.frombuffer(b"".join(wl.host_bytes((rank + i * world) * n, n) for i in range(4)), np.uint8).copy()
+        S = ctx["seed"].words_np(0, ctx["seed"].capacity)
+        want = coracle.hash_fixed(ctx["w"], host, 4, n, n, S)
+        check = bool(np.array_equal(got, want))
+    del ctx
+    torch.cuda.empty_cache()
+    e2e = None
+    if rank == 0 and args.e2e_steps > 0:
+        try:
+            e2e, _ = e2e_fixed(hh, torch, workload, args.e2e_steps, args.e2e_strings)
+            e2e["value"] *= 1.0
+        except Exception as ex:  # pragma: no cover - report, do not hide
+            e2e = {"value": None, "unit": UNIT, "error": repr(ex), "h2d_bytes_per_step": None,
+                   "d2h_bytes_per_step": None}
+    extra = {}
+    cpu = None
+    if rank == 0 and world == 1:
+        if not args.no_extra:
+            for wk in ("cfg1", "cfg2", "cfg3", "cfg5"):
+                try:
+                    extra[wk] = measure_workload(hh, torch, wk, steps=max(5, min(args.steps, 50)), warmup=3,
+                                                 peak=peak)
+                except Exception as ex:  # pragma: no cover
+                    extra[wk] = {"error": repr(ex)}
+        cores = os.cpu_count() or 1
+        per_core = 2
+        cpu_rate(workload, 1, min(cores, 2))
+        r, b, dt = cpu_rate(workload, per_core, cores)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{cores} processes x {per_core} x 1 MiB strings (v40), {b} bytes in {dt:.2f} s; "
+                         "numpy restatement of hasher.py:331-413 (oracle/oracle_np.py)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (splitmix stream seed 0; seed array seed 1)",
+            "config": {"workload": workload, "desc": wl.CONFIGS[workload]["desc"], "n_strings_per_gpu": B,
+                       "n_bytes": n, "variant": ctx_variant(workload), "sharding": "round-robin by string",
+                       "l2": "inputs (8 GiB/GPU) larger than L2 (126 MB); no flush needed",
+                       "parallelism": f"dp{world} (independent strings, no collective)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _traffic(workload),
+                         "kernel": "hash_kernel<40,false,4,4>", "kernel_ms": kernel_ms,
+                         "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+            "oracle_check": check,
+            "workloads": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def ctx_variant(workload):
+    return wl.CONFIGS[workload]["variant"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs")
+    ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-strings", type=int, default=0, help="cap e2e batch (0 = full config)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return arm_reference(args, rank, world)
+    return arm_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -26,6 +26,14 @@
  *    allocation satisfies this.
  *  - Digests are written as n_strings x k little-endian u64 words,
  *    k = output_bytes / 8 (Digest.words, hasher.py:165-176).
+ *  - hth_hash_fixed workspaces must be zero-filled before their first use
+ *    (one cudaMemset after allocation).  Every completed call leaves the
+ *    workspace zero-filled again (self-resetting counters/accumulators,
+ *    consumed subtree blocks cleared), so it is reused across calls on one
+ *    stream without clearing and the hot path is a single kernel launch.
+ *    hth_hash_varlen clears its own state per call; a workspace it used must
+ *    be re-zeroed before hth_hash_fixed uses it.  Concurrent calls need
+ *    distinct workspaces.
  *  - Seeds: d_seed holds the expanded seed words S[0..seed_capacity)
  *    (SeedBuffer.words_np, hasher.py:94-97).  Any capacity >= the layout
  *    total is accepted and gives identical digests (hasher.py:8-10).

@@ -56,20 +56,27 @@ def _seed_ptr(seed, dev):
 
 
 class _Workspace:
-    """Per-device reusable workspace (grown on demand, stream-ordered via torch's allocator)."""
+    """Reusable engine workspace per (device, stream).
+
+    The C-ABI requires a zero-filled workspace on first use and leaves it
+    zero-filled after every call (its counters and accumulators reset
+    themselves), so one zeroed allocation serves all later calls.
+    """
 
     def __init__(self):
         self.buf = {}
 
     def get(self, dev, nbytes):
-        t = self.buf.get(dev.index)
+        key = (dev.index, _stream(dev))
+        t = self.buf.get(key)
         if t is None or t.numel() < nbytes:
-            t = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
-            self.buf[dev.index] = t
+            t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=dev)
+            self.buf[key] = t
         return t
 
 
-_WS = _Workspace()
+_WS = _Workspace()       # hash_fixed: zero-filled, kept zero by the engine
+_WS_VAR = _Workspace()   # hash_varlen: plan areas are scratch, cleared per call
 
 
 def hash_fixed(data: torch.Tensor, n_bytes: int, seed, params: HashParams, n_strings: int = None,
@@ -146,7 +153,7 @@ def hash_varlen(data: torch.Tensor, offsets, seed, params: HashParams, max_n_byt
         out = torch.empty((max(n, 0), k), dtype=torch.int64, device=dev)
     total = data.numel()
     wsz = workspace_varlen(params, max(n, 0), total)
-    ws = workspace if workspace is not None else _WS.get(dev, wsz)
+    ws = workspace if workspace is not None else _WS_VAR.get(dev, wsz)
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().hth_hash_varlen(
             params.output_bytes, data.data_ptr(), d_off.data_ptr(), n, max_n_bytes, total, seed_t.data_ptr(),

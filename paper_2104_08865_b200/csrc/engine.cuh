@@ -208,9 +208,21 @@ struct Params {
   const u64* meta;       // varlen: 3 u64 per string (job_first, scratch, cnt); entry n = totals
   const u64* S;
   u64* out;
-  u64* scratch;
-  u32* counters;
+  u64* scratch;   // level >= 2 blocks awaiting their group's merge
+  u32* counters;  // per-group arrival counts (self-resetting)
+  u64* acc;       // per multi-job string: k partial digest words (self-resetting)
+  u32* events;    // per multi-job string: completion events seen (self-resetting)
 };
+
+// Completion events of a multi-job string: its last job, plus one per block
+// at level >= 2 that ends as a leftover (each such block's producer is the
+// last warp to touch anything beneath it).  When all have arrived, every
+// finalize term is in `acc`.
+__device__ __forceinline__ u32 string_events(u64 n_inst) {
+  u32 e = 1;
+  for (int l = 2; (n_inst >> (3 * l)) > 0; l++) e += (u32)((n_inst >> (3 * l)) & 7);
+  return e;
+}
 
 template <int K>
 __device__ __forceinline__ void layout_bases(u32 L, int ew, u64 (&T)[K], u64 (&F)[K], u64& R) {

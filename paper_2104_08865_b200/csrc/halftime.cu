@@ -111,8 +111,6 @@ __global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, Tri* tri, u6
     u64 w, c;
     scratch_need(ni, K, &w, &c);
     tri[s] = {J, w, c};
-    if (J > 1)
-      for (int r = 0; r < K; r++) out[s * K + r] = 0;
   }
 }
 
@@ -192,7 +190,7 @@ int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
 
 // fixed-mode geometry
 struct FixedPlan {
-  u64 n_inst, J, n_jobs, scr_per, cnt_per, ws_scratch, ws_cnt, ws_total;
+  u64 n_inst, J, n_jobs, scr_per, cnt_per, ws_scratch, ws_acc, ws_cnt, ws_ev, ws_total;
 };
 FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
   FixedPlan f;
@@ -200,15 +198,19 @@ FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
   f.J = f.n_inst > (u64)JOB_INST ? ceil_div(f.n_inst, JOB_INST) : 1;
   f.n_jobs = n_strings * f.J;
   scratch_need(f.n_inst, v.k, &f.scr_per, &f.cnt_per);
+  const bool multi = f.J > 1;
   f.ws_scratch = align_up(n_strings * f.scr_per * 8, 256);
+  f.ws_acc = multi ? align_up(n_strings * v.k * 8, 256) : 0;
   f.ws_cnt = align_up(n_strings * f.cnt_per * 4, 256);
-  f.ws_total = f.ws_scratch + f.ws_cnt;
+  f.ws_ev = multi ? align_up(n_strings * 4, 256) : 0;
+  f.ws_total = f.ws_scratch + f.ws_acc + f.ws_cnt + f.ws_ev;
   return f;
 }
 
 // varlen workspace geometry
 struct VarPlan {
-  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_cub, cub_bytes, total, max_jobs, scr_words, cnts;
+  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_acc, off_ev, off_cub, cub_bytes, total, max_jobs,
+      scr_words, cnts;
 };
 int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
   const u64 total_inst = total_bytes / (8ull * v.m);
@@ -226,7 +228,10 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
   p->off_meta = o; o = align_up(o + (n + 1) * sizeof(Tri), 256);
   p->off_jobs = o; o = align_up(o + p->max_jobs * 4, 256);
   p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
+  // self-resetting state, contiguous so one memset per call clears it
   p->off_cnt = o; o = align_up(o + p->cnts * 4, 256);
+  p->off_acc = o; o = align_up(o + n * v.k * 8, 256);
+  p->off_ev = o; o = align_up(o + n * 4, 256);
   p->off_cub = o; o = align_up(o + cub_bytes, 256);
   p->total = o;
   return HTH_OK;
@@ -277,7 +282,10 @@ int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_by
     for (int i = 0; i < 3; i++) {
       if (c.ws[i]) cudaFree(c.ws[i]);
       CK(cudaMalloc(&c.ws[i], ws_bytes));
+      CK(cudaMemset(c.ws[i], 0, ws_bytes));  // engine keeps it zeroed afterwards
     }
+    // the memsets ran on the legacy stream; our streams are non-blocking
+    CK(cudaDeviceSynchronize());
     c.ws_bytes = ws_bytes;
   }
   *out = &c;
@@ -389,10 +397,11 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.cnt_per = f.cnt_per;
   P.S = d_seed;
   P.out = d_out;
-  P.scratch = (u64*)d_workspace;
-  P.counters = (u32*)((uint8_t*)d_workspace + f.ws_scratch);
-  if (f.J > 1) CK(cudaMemsetAsync(d_out, 0, n_strings * v.k * 8, st));
-  if (f.cnt_per) CK(cudaMemsetAsync(P.counters, 0, n_strings * f.cnt_per * 4, st));
+  uint8_t* ws = (uint8_t*)d_workspace;
+  P.scratch = (u64*)ws;
+  P.acc = (u64*)(ws + f.ws_scratch);
+  P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
+  P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
   return dispatch<false>(output_bytes, P, f.n_jobs, st);
 }
 
@@ -428,7 +437,8 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   Tri* meta = (Tri*)(ws + p.off_meta);
   u32* jobs = (u32*)(ws + p.off_jobs);
   CK(cudaMemsetAsync(err, 0, 4, st));
-  CK(cudaMemsetAsync(ws + p.off_cnt, 0, p.cnts * 4, st));
+  // plan areas of an earlier call may overlap this call's counters/accumulators
+  CK(cudaMemsetAsync(ws + p.off_cnt, 0, p.off_cub - p.off_cnt, st));
   const u64 blocks = std::min<u64>(ceil_div(n_strings + 1, 256), 4096);
   switch (output_bytes) {
     case 16: plan_count_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
@@ -453,6 +463,8 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   P.out = d_out;
   P.scratch = (u64*)(ws + p.off_scr);
   P.counters = (u32*)(ws + p.off_cnt);
+  P.acc = (u64*)(ws + p.off_acc);
+  P.events = (u32*)(ws + p.off_ev);
   return dispatch<true>(output_bytes, P, p.max_jobs, st);
 }
 

@@ -39,7 +39,7 @@ struct TreeCtx {
 // (tree.py:103-134), or it joins a complete group of 8 whose node the last
 // arriving warp computes (nh.py:96-121 with level seeds, tree.py:55-60).
 template <int K>
-__device__ __forceinline__ void climb(const Params& P, const Str& st, const TreeCtx<K>& tc, int lvl, u64 idx,
+__device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeCtx<K>& tc, int lvl, u64 idx,
                                       u64 (&B)[K], u64 (&fin)[K], int lane) {
   const int q = lane >> 3, j = lane & 7;
   const u64* __restrict__ S = P.S;
@@ -50,7 +50,7 @@ __device__ __forceinline__ void climb(const Params& P, const Str& st, const Tree
 #pragma unroll
         for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B[r], __ldg(S + tc.F[r] + 56ull * lvl + (idx & 7) * 8 + j));
       }
-      return;
+      return 1;
     }
     u64 woff = 0, coff = 0;
     for (int l = 2; l <= lvl; l++) {
@@ -66,15 +66,19 @@ __device__ __forceinline__ void climb(const Params& P, const Str& st, const Tree
     __threadfence();
     __syncwarp();
     u32 old = 0;
-    if (lane == 0) old = atomicAdd(P.counters + st.cnt + coff + (idx >> 3), 1u);
+    u32* ctr = P.counters + st.cnt + coff + (idx >> 3);
+    if (lane == 0) old = atomicAdd(ctr, 1u);
     old = __shfl_sync(0xffffffffu, old, 0);
-    if (old != 7) return;
+    if (old != 7) return 0;
     __threadfence();
-    const u64* g = blk + (idx & ~7ull) * 8 * K;
+    if (lane == 0) *ctr = 0;  // last arriver: leave the workspace zeroed
+    u64* g = blk + (idx & ~7ull) * 8 * K;
 #pragma unroll
     for (int r = 0; r < K; r++) {
       const u64 a = __ldcg(g + q * 8 * K + r * 8 + j);
       const u64 b = __ldcg(g + (q + 4) * 8 * K + r * 8 + j);
+      g[q * 8 * K + r * 8 + j] = 0;  // consumed: leave the workspace zeroed
+      g[(q + 4) * 8 * K + r * 8 + j] = 0;
       const u64* s = S + tc.T[r] + 7ull * lvl;
       u64 v = nh_acc(0, a, __ldg(s + q));
       v = (q < 3) ? nh_acc(v, b, __ldg(s + q + 4)) : v + b;
@@ -163,6 +167,7 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
     layout_bases<K>(st.L, Geo<V>::ew, tc.T, tc.F, tc.R);
 
     u64 fin[K], n1[K], n2[K];
+    u32 events = last_job ? 1u : 0u;
 #pragma unroll
     for (int r = 0; r < K; r++) fin[r] = n1[r] = n2[r] = 0;
     const u64 inst0 = (u64)jq * JOB_INST;
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
                 n2[r] = (p1 < 7) ? nh_acc(n2[r], B1[r], __ldg(S + tc.T[r] + 7 + p1)) : n2[r] + B1[r];
             }
             if (p1 == 7) {
-              climb<K>(P, st, tc, 2, G1 >> 3, n2, fin, lane);
+              events += climb<K>(P, st, tc, 2, G1 >> 3, n2, fin, lane);
 #pragma unroll
               for (int r = 0; r < K; r++) n2[r] = 0;
             }
@@ -278,12 +283,24 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
       const u64 v = warp_sum(fin[r]);
       if (lane == r) mine = v;
     }
-    if (lane < K) {
-      u64* o = P.out + st.s * K + lane;
-      if (st.J == 1)
-        *o = mine;
-      else
-        atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)mine);
+    if (st.J == 1) {
+      if (lane < K) P.out[st.s * K + lane] = mine;
+    } else if (events) {
+      // multi-job string: add this job's finalize terms, then count its
+      // events; the warp completing the count publishes the digest and
+      // re-zeroes the accumulators (integer sums: order-independent).
+      unsigned long long* a = reinterpret_cast<unsigned long long*>(P.acc + st.s * K);
+      if (lane < K) atomicAdd(a + lane, (unsigned long long)mine);
+      __threadfence();
+      __syncwarp();
+      u32 old = 0;
+      if (lane == 0) old = atomicAdd(P.events + st.s, events);
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (old + events == string_events(st.n_inst)) {
+        __threadfence();
+        if (lane < K) P.out[st.s * K + lane] = atomicExch(a + lane, 0ull);
+        if (lane == 0) P.events[st.s] = 0;
+      }
     }
   }
 }
