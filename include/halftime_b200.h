@@ -34,9 +34,13 @@
  *    hth_hash_varlen clears its own state per call; a workspace it used must
  *    be re-zeroed before hth_hash_fixed uses it.  Concurrent calls need
  *    distinct workspaces.
- *  - Seeds: d_seed holds the expanded seed words S[0..seed_capacity)
- *    (SeedBuffer.words_np, hasher.py:94-97).  Any capacity >= the layout
- *    total is accepted and gives identical digests (hasher.py:8-10).
+ *  - Seeds (SeedBuffer, hasher.py:70-102): seed_fold is the master fold
+ *    (hth_master_fold) and d_seed holds its expansion S[0..seed_capacity)
+ *    (hth_expand_seed(seed_fold, 0, seed_capacity, d_seed), i.e.
+ *    SeedBuffer.words_np).  The first e*w words are recomputed from the fold
+ *    on the host and travel in the kernel's constant-bank parameters; the
+ *    rest are read from d_seed.  Any capacity >= the layout total is
+ *    accepted and gives identical digests (hasher.py:8-10).
  */
 #ifndef HALFTIME_B200_H
 #define HALFTIME_B200_H
@@ -90,8 +94,8 @@ int hth_fill_splitmix(uint64_t fill_seed, uint64_t word_offset, uint64_t n_bytes
  * hth_workspace_size_fixed() bytes of device memory (NULL if that is 0). */
 int hth_workspace_size_fixed(int output_bytes, uint64_t n_strings, uint64_t n_bytes, uint64_t* bytes);
 int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uint64_t stride_bytes,
-                   uint64_t n_bytes, const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out,
-                   void* d_workspace, uint64_t workspace_bytes, void* stream);
+                   uint64_t n_bytes, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
+                   uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes, void* stream);
 
 /* ---- batched hash of variable-length strings packed in one buffer.
  * String s is d_data[d_offsets[s] .. d_offsets[s+1]) (u64 byte offsets on the
@@ -101,8 +105,9 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
  * workspace (>= d_offsets[n] - d_offsets[0]). */
 int hth_workspace_size_varlen(int output_bytes, uint64_t n_strings, uint64_t total_bytes, uint64_t* bytes);
 int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offsets, uint64_t n_strings,
-                    uint64_t max_n_bytes, uint64_t total_bytes, const uint64_t* d_seed, uint64_t seed_capacity,
-                    uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes, void* stream);
+                    uint64_t max_n_bytes, uint64_t total_bytes, uint64_t seed_fold, const uint64_t* d_seed,
+                    uint64_t seed_capacity, uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes,
+                    void* stream);
 /* Synchronizes `stream`; returns HTH_ESEEDSIZE if the last varlen call on this
  * workspace met a string longer than its max_n_bytes, else HTH_OK. */
 int hth_varlen_status(void* d_workspace, void* stream);

@@ -55,9 +55,9 @@ def lib() -> ctypes.CDLL:
             "hth_expand_seed": [u64, u64, u64, vp, vp],
             "hth_fill_splitmix": [u64, u64, u64, vp, vp],
             "hth_workspace_size_fixed": [i32, u64, u64, pu64],
-            "hth_hash_fixed": [i32, vp, u64, u64, u64, vp, u64, vp, vp, u64, vp],
+            "hth_hash_fixed": [i32, vp, u64, u64, u64, u64, vp, u64, vp, vp, u64, vp],
             "hth_workspace_size_varlen": [i32, u64, u64, pu64],
-            "hth_hash_varlen": [i32, vp, vp, u64, u64, u64, vp, u64, vp, vp, u64, vp],
+            "hth_hash_varlen": [i32, vp, vp, u64, u64, u64, u64, vp, u64, vp, vp, u64, vp],
             "hth_varlen_status": [vp, vp],
             "hth_hash_host": [i32, vp, u64, ctypes.c_char_p, u64, vp, i32],
             "hth_hash_fixed_host": [i32, vp, u64, u64, u64, ctypes.c_char_p, u64, vp, i32],

@@ -44,15 +44,10 @@ def workspace_varlen(params: HashParams, n_strings: int, total_bytes: int) -> in
 
 
 def _seed_ptr(seed, dev):
-    """(pointer, capacity) of device seed words: a SeedBuffer or an int64/uint64 CUDA tensor."""
+    """(device words, capacity, fold) of a SeedBuffer (hasher.py:70-97)."""
     if isinstance(seed, SeedBuffer):
-        t = seed.device_words(dev)
-        return t, seed.capacity
-    if isinstance(seed, torch.Tensor):
-        if not seed.is_cuda or seed.element_size() != 8:
-            raise ValueError("seed tensor must be a CUDA 64-bit tensor")
-        return seed, seed.numel()
-    raise ValueError("seed must be a SeedBuffer or a CUDA tensor of seed words")
+        return seed.device_words(dev), seed.capacity, seed.fold
+    raise ValueError("seed must be a SeedBuffer (expand_seed / seed_for_input)")
 
 
 class _Workspace:
@@ -103,9 +98,8 @@ def hash_fixed(data: torch.Tensor, n_bytes: int, seed, params: HashParams, n_str
         stride = n_bytes if stride is None else stride
     if n_strings and (n_strings - 1) * stride + n_bytes > data.numel():
         raise ValueError("data tensor too small for n_strings * stride")
-    seed_t, cap = _seed_ptr(seed, dev)
-    if isinstance(seed, SeedBuffer):
-        _check_capacity(seed, params, n_bytes)
+    seed_t, cap, fold = _seed_ptr(seed, dev)
+    _check_capacity(seed, params, n_bytes)
     k = params.output_words
     if out is None:
         out = torch.empty((n_strings, k), dtype=torch.int64, device=dev)
@@ -113,7 +107,7 @@ def hash_fixed(data: torch.Tensor, n_bytes: int, seed, params: HashParams, n_str
     ws = workspace if workspace is not None else (_WS.get(dev, wsz) if wsz else None)
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().hth_hash_fixed(
-            params.output_bytes, data.data_ptr(), n_strings, stride, n_bytes, seed_t.data_ptr(), cap,
+            params.output_bytes, data.data_ptr(), n_strings, stride, n_bytes, fold, seed_t.data_ptr(), cap,
             out.data_ptr(), ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
             _stream(dev)))
     return out
@@ -145,9 +139,8 @@ def hash_varlen(data: torch.Tensor, offsets, seed, params: HashParams, max_n_byt
             max_n_bytes = int(np.max(off[1:] - off[:-1])) if off.size > 1 else 0
         d_off = torch.from_numpy(off.view(np.int64)).to(dev, non_blocking=False)
     n = d_off.numel() - 1
-    seed_t, cap = _seed_ptr(seed, dev)
-    if isinstance(seed, SeedBuffer):
-        _check_capacity(seed, params, max_n_bytes)
+    seed_t, cap, fold = _seed_ptr(seed, dev)
+    _check_capacity(seed, params, max_n_bytes)
     k = params.output_words
     if out is None:
         out = torch.empty((max(n, 0), k), dtype=torch.int64, device=dev)
@@ -156,7 +149,7 @@ def hash_varlen(data: torch.Tensor, offsets, seed, params: HashParams, max_n_byt
     ws = workspace if workspace is not None else _WS_VAR.get(dev, wsz)
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().hth_hash_varlen(
-            params.output_bytes, data.data_ptr(), d_off.data_ptr(), n, max_n_bytes, total, seed_t.data_ptr(),
+            params.output_bytes, data.data_ptr(), d_off.data_ptr(), n, max_n_bytes, total, fold, seed_t.data_ptr(),
             cap, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(dev)))
     return out
 

@@ -1,30 +1,35 @@
-// HalftimeHash B200 engine: device side.
+// HalftimeHash B200 engine: device-side building blocks.
 //
 // One kernel hashes a batch of strings.  Work is cut into warp JOBS: job
-// (s, jq) covers instances [64 jq, 64 jq + 64) of string s (one level-2
-// subtree of the reference's stack construction, tree.py:63-100), and the
-// string's last job also covers its Toeplitz tail (hasher.py:407-412).
+// (s, jq) covers instances [8^L jq, 8^L (jq + 1)) of string s, L = job_lvl
+// (2 or 3): one level-L subtree of the reference's stack construction
+// (tree.py:63-100).  The string's last job also covers its Toeplitz tail
+// (hasher.py:407-412).
 //
 // Per warp: a ring of NS shared-memory stages fed by cp.async.bulk (TMA 1-D
-// bulk copies completing on an mbarrier).  A stage holds one ROUND = 4
-// instances (plus the tail in the string's last round).  Thread (q, j) of
-// the warp (q = lane / 8, j = lane % 8) owns lane j of instance 4c + q:
+// bulk copies completing on an mbarrier).  A stage holds one ROUND = 8
+// instances = one level-1 group (plus the tail in the string's last round).
+// Thread (q, j) of the warp (q = lane / 8, j = lane % 8) owns lane j of
+// instances 8c + q and 8c + q + 4:
 //   encode (GF(16) Cauchy / XOR parity, ehc.py:23-46) -> NH (ehc.py:49-72)
-//   -> combine (ehc.py:75-99), all in registers.
+//   -> combine (ehc.py:75-99), all in registers.  For the Cauchy variants
+// the two instances are packed plane-by-plane into shared 32-bit registers
+// so every XOR of the encode advances 32 GF(16) elements.
 // Level-1 nodes (nh.py:96-121) are reduced over the 4 threads sharing j
-// with two shuffles; level-2 nodes accumulate serially in lanes 0-7.
-// Levels >= 3 use a "last arriver" merge through a global scratch area.
+// with two shuffles; levels 2..L accumulate serially in lanes 0-7; levels
+// >= L use a "last arriver" merge through a global scratch area.
 //
 // The reference's finalize (tree.py:103-134) is a plain sum of NH terms
 // over leftover slots, zero slots and the length tag; the tail is a sum of
 // NH terms too.  Every block that ends up a leftover therefore adds its
-// finalize terms straight into the digest accumulator the moment it is
-// produced; digests of multi-job strings are summed with 64-bit atomics
-// (integer, mod 2^64: order-independent, so bit-exact and deterministic).
+// finalize terms into the digest accumulator the moment it is produced;
+// integer sums mod 2^64 are order-independent, so the result is bit-exact
+// and deterministic however the warps interleave.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "encode_gen.cuh"
 #include "variants.cuh"
 
 namespace hth {
@@ -32,8 +37,8 @@ namespace hth {
 typedef uint64_t u64;
 typedef uint32_t u32;
 
-constexpr int JOB_INST = 64;   // instances per warp job (8^2)
-constexpr int ROUND_INST = 4;  // instances per stage
+constexpr int ROUND_INST = 8;  // instances per stage: one level-1 group
+constexpr int MAX_EW = 30;     // max e*w over the variants (v32: 10 * 3)
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -80,16 +85,30 @@ struct w2 {
   u32 lo, hi;
 };
 __device__ __forceinline__ w2 mk(u64 x) { return {(u32)x, (u32)(x >> 32)}; }
-__device__ __forceinline__ u64 cat(w2 a) { return ((u64)a.hi << 32) | a.lo; }
 __device__ __forceinline__ w2 operator^(w2 a, w2 b) { return {a.lo ^ b.lo, a.hi ^ b.hi}; }
 
 // NH(x, s) = ((x_lo + s_lo) mod 2^32) * ((x_hi + s_hi) mod 2^32)  (nh.py:48-67)
 // acc + (u64)a*b lowers to one IMAD.WIDE.U32.
-__device__ __forceinline__ u64 nh_acc(u64 acc, w2 x, u64 s) {
-  u32 a = x.lo + (u32)s, b = x.hi + (u32)(s >> 32);
-  return acc + (u64)a * b;
-}
+__device__ __forceinline__ u64 nh_acc(u64 acc, w2 x, u32 slo, u32 shi) { return acc + (u64)(x.lo + slo) * (x.hi + shi); }
+__device__ __forceinline__ u64 nh_acc(u64 acc, w2 x, u64 s) { return nh_acc(acc, x, (u32)s, (u32)(s >> 32)); }
 __device__ __forceinline__ u64 nh_acc(u64 acc, u64 x, u64 s) { return nh_acc(acc, mk(x), s); }
+
+// acc += C * h (mod 2^64) for a small constant C in two IMADs: the low half
+// as one IMAD.WIDE.U32 (carry included), the high half as one IMAD.
+template <int C>
+__device__ __forceinline__ u64 mac_const(u64 acc, u64 h) {
+  if (C == 0) return acc;
+  u64 r;
+  asm("{\n .reg .u32 lo, hi, hl, hh;\n"
+      " mov.b64 {hl, hh}, %2;\n"
+      " mad.wide.u32 %0, hl, %3, %1;\n"
+      " mov.b64 {lo, hi}, %0;\n"
+      " mad.lo.u32 hi, hh, %3, hi;\n"
+      " mov.b64 %0, {lo, hi};\n}"
+      : "=l"(r)
+      : "l"(acc), "l"(h), "n"(C));
+  return r;
+}
 
 // x * v on 16 bit-sliced GF(16) elements (gf16.py:17-21), in 32-bit halves:
 // lo = planes 0,1; hi = planes 2,3.  2 PRMT + 1 LOP3.
@@ -110,50 +129,12 @@ __device__ __forceinline__ u64 warp_sum(u64 v) {
   return v;
 }
 
-// ------------------------------------------------------------ EHC leaf
-// X[i][u] = lane word of input item i, block u.  Returns C[r], r < k
-// (hasher.py:356-364; ehc.py:102-118).  Encode uses the Horner form of
-// gf16.scale: sum_i c_i * X_i = Q0 ^ x(Q1 ^ x(Q2 ^ x Q3)), Q_b = XOR of X_i
-// whose coefficient has bit b set (xtime is GF(2)-linear).
-template <class V>
-__device__ __forceinline__ void leaf(const w2 (&X)[V::d][V::w], const u64* __restrict__ S, u64 (&C)[V::k]) {
-#pragma unroll
-  for (int r = 0; r < V::k; r++) C[r] = 0;
-#pragma unroll
-  for (int i = 0; i < V::e; i++) {
-    u64 h = 0;
-#pragma unroll
-    for (int u = 0; u < V::w; u++) {
-      w2 E;
-      if (i < V::d) {
-        E = X[i][u];
-      } else {
-        w2 q[4] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-#pragma unroll
-        for (int t = 0; t < V::d; t++) {
-          const int c = V::par(i - V::d, t);
-#pragma unroll
-          for (int b = 0; b < 4; b++)
-            if ((c >> b) & 1) q[b] = q[b] ^ X[t][u];
-        }
-        E = q[0] ^ xtime(q[1] ^ xtime(q[2] ^ xtime(q[3])));
-      }
-      h = nh_acc(h, E, __ldg(S + i * V::w + u));
-    }
-#pragma unroll
-    for (int r = 0; r < V::k; r++) {
-      const int c = V::mat(r, i);
-      if (c) C[r] += (u64)c * h;
-    }
-  }
-}
-
 // ------------------------------------------------------------ per-string view
 struct Str {
   const uint8_t* p;  // first byte (global)
   u64 n;             // bytes
   u64 n_inst;        // full instances
-  u32 L;             // leftover levels (layout levels, >= 1)
+  u32 L;             // layout levels (>= 1)
   u32 J;             // warp jobs
   u64 scratch;       // base word of this string's scratch blocks
   u64 cnt;           // base index of this string's counters
@@ -170,59 +151,57 @@ __host__ __device__ __forceinline__ u32 level_count(u64 n) {
 }
 __host__ __device__ __forceinline__ u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 
-// scratch words / counters a string needs for merges above level 2
-__host__ __device__ __forceinline__ void scratch_need(u64 n_inst, int k, u64* words, u64* cnts) {
+// jobs of a string: one per 8^job_lvl instances (at least one)
+__host__ __device__ __forceinline__ u64 job_count(u64 n_inst, int job_lvl) {
+  const u64 per = 1ull << (3 * job_lvl);
+  return n_inst > per ? ceil_div(n_inst, per) : 1;
+}
+
+// scratch words / counters a string needs for merges above the job level
+__host__ __device__ __forceinline__ void scratch_need(u64 n_inst, int k, int job_lvl, u64* words, u64* cnts) {
   u64 w = 0, c = 0;
-  for (int l = 2; (n_inst >> (3 * l)) >= 8; l++) {
-    u64 len = n_inst >> (3 * l);
+  for (int l = job_lvl; (n_inst >> (3 * l)) >= 8; l++) {
+    const u64 len = n_inst >> (3 * l);
     w += (len & ~7ull) * 8ull * k;
     c += len >> 3;
   }
   *words = w;
   *cnts = c;
 }
-// offset of level `lvl` blocks inside the string's scratch, and of the
-// counters of level `lvl` nodes (lvl >= 3) inside its counter area
-__device__ __forceinline__ void scratch_off(u64 n_inst, int k, int lvl, u64* woff, u64* coff) {
-  u64 w = 0, c = 0;
-  for (int l = 2; l < lvl; l++) {
-    u64 len = n_inst >> (3 * l);
-    w += (len & ~7ull) * 8ull * k;
-    if (l >= 3) c += len;
-  }
-  *woff = w;
-  *coff = c;
+
+// Completion events of a multi-job string: its last job, plus one per block
+// at level >= job_lvl that ends as a leftover (each such block's producer
+// is the last warp to touch anything beneath it).  When all have arrived,
+// every finalize term is in the accumulator.
+__host__ __device__ __forceinline__ u32 string_events(u64 n_inst, int job_lvl) {
+  u32 e = 1;
+  for (int l = job_lvl; (n_inst >> (3 * l)) > 0; l++) e += (u32)((n_inst >> (3 * l)) & 7);
+  return e;
 }
 
 struct Params {
   const uint8_t* data;
   u64 n_strings;
-  u64 stride;      // fixed mode
-  u64 n_bytes;     // fixed mode
-  u64 J_fixed;     // fixed mode: jobs per string
-  u64 n_jobs;      // fixed mode: total jobs
-  u64 scr_per;     // fixed mode: scratch words per string
-  u64 cnt_per;     // fixed mode: counters per string
-  const u64* offsets;    // varlen: n_strings + 1 byte offsets
-  const u32* job_str;    // varlen: job -> string
-  const u64* meta;       // varlen: 3 u64 per string (job_first, scratch, cnt); entry n = totals
-  const u64* S;
+  u64 stride;    // fixed mode
+  u64 n_bytes;   // fixed mode: length; varlen: length clamp (host-checked bound)
+  u64 J_fixed;   // fixed mode: jobs per string
+  u64 n_jobs;    // fixed mode: total jobs
+  u64 scr_per;   // fixed mode: scratch words per string
+  u64 cnt_per;   // fixed mode: counters per string
+  const u64* offsets;  // varlen: n_strings + 1 byte offsets
+  const u32* job_str;  // varlen: job -> string
+  const u64* meta;     // varlen: 3 u64 per string (job_first, scratch, cnt); entry n = totals
+  const u64* S;        // expanded seed words (SeedBuffer.words_np)
   u64* out;
-  u64* scratch;   // level >= 2 blocks awaiting their group's merge
+  u64* scratch;   // level >= job_lvl blocks awaiting their group's merge
   u32* counters;  // per-group arrival counts (self-resetting)
   u64* acc;       // per multi-job string: k partial digest words (self-resetting)
   u32* events;    // per multi-job string: completion events seen (self-resetting)
+  int job_lvl;    // a warp job is one level-`job_lvl` subtree
+  // EHC seed words S[0..e*w), split into halves.  The kernel takes Params as
+  // a __grid_constant__, so these are constant-bank operands of the NH adds.
+  u32 ehc_lo[MAX_EW], ehc_hi[MAX_EW];
 };
-
-// Completion events of a multi-job string: its last job, plus one per block
-// at level >= 2 that ends as a leftover (each such block's producer is the
-// last warp to touch anything beneath it).  When all have arrived, every
-// finalize term is in `acc`.
-__device__ __forceinline__ u32 string_events(u64 n_inst) {
-  u32 e = 1;
-  for (int l = 2; (n_inst >> (3 * l)) > 0; l++) e += (u32)((n_inst >> (3 * l)) & 7);
-  return e;
-}
 
 template <int K>
 __device__ __forceinline__ void layout_bases(u32 L, int ew, u64 (&T)[K], u64 (&F)[K], u64& R) {
@@ -239,7 +218,7 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u3
   u64 s;
   if (VARLEN) {
     s = P.job_str[job];
-    u64 o0 = P.offsets[s], o1 = P.offsets[s + 1];
+    const u64 o0 = P.offsets[s], o1 = P.offsets[s + 1];
     st.p = P.data + o0;
     st.n = min(o1 - o0, P.n_bytes);  // clamp to the host-checked bound (plan_count_kernel)
     const u64* mt = P.meta + 3 * s;
@@ -257,14 +236,15 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u3
   st.s = s;
   st.n_inst = ((st.n + 7) >> 3) / M;
   st.L = st.n_inst ? level_count(st.n_inst) : 1;
-  st.J = st.n_inst > (u64)JOB_INST ? (u32)ceil_div(st.n_inst, JOB_INST) : 1;
+  st.J = (u32)job_count(st.n_inst, P.job_lvl);
 }
 
 // bytes of job jq (its instances, plus the tail for the last job)
 template <int M>
-__device__ __forceinline__ void job_span(const Str& st, u32 jq, u64& byte0, u64& nbytes, u32& ninst) {
-  u64 i0 = (u64)jq * JOB_INST;
-  u64 ni = st.n_inst > i0 ? min((u64)JOB_INST, st.n_inst - i0) : 0;
+__device__ __forceinline__ void job_span(const Str& st, u32 jq, int job_lvl, u64& byte0, u64& nbytes, u32& ninst) {
+  const u64 per = 1ull << (3 * job_lvl);
+  const u64 i0 = (u64)jq * per;
+  const u64 ni = st.n_inst > i0 ? min(per, st.n_inst - i0) : 0;
   ninst = (u32)ni;
   byte0 = i0 * (M * 8ull);
   nbytes = (jq + 1 == st.J) ? st.n - byte0 : ni * (M * 8ull);

@@ -62,6 +62,27 @@ int get_var(int out, VarInfo* v) {
   return HTH_OK;
 }
 
+// EHC seed words S[0..e*w) = mix(fold + (i+1) gamma) (hasher.py:55-58),
+// passed to the kernel in its constant-bank parameters
+u64 host_mix(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+void fill_ehc(const VarInfo& v, u64 fold, Params& P) {
+  for (int i = 0; i < v.ew; i++) {
+    const u64 w = host_mix(fold + (u64)(i + 1) * 0x9E3779B97F4A7C15ull);
+    P.ehc_lo[i] = (u32)w;
+    P.ehc_hi[i] = (u32)(w >> 32);
+  }
+}
+
+u64 fold_of(const uint8_t* m) {
+  u64 w[4];
+  memcpy(w, m, 32);
+  return w[0] ^ w[1] ^ w[2] ^ w[3];
+}
+
 // ------------------------------------------------------------ kernels (aux)
 __device__ __forceinline__ u64 mix64(u64 z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -94,7 +115,7 @@ struct TriSum {
 };
 
 template <int OUT>
-__global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, Tri* tri, u64* out, int* err) {
+__global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, int job_lvl, Tri* tri, int* err) {
   constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m;
   for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s <= n; s += (u64)gridDim.x * blockDim.x) {
     if (s == n) {
@@ -107,9 +128,9 @@ __global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, Tri* tri, u6
       nb = max_n;
     }
     const u64 ni = ((nb + 7) >> 3) / M;
-    const u64 J = ni > (u64)JOB_INST ? ceil_div(ni, JOB_INST) : 1;
+    const u64 J = job_count(ni, job_lvl);
     u64 w, c;
-    scratch_need(ni, K, &w, &c);
+    scratch_need(ni, K, job_lvl, &w, &c);
     tri[s] = {J, w, c};
   }
 }
@@ -123,10 +144,12 @@ __global__ void plan_fill_kernel(const Tri* meta, u64 n, u32* job_str) {
 
 // ------------------------------------------------------------ launch config
 template <int OUT> struct KCfg;
-template <> struct KCfg<16> { static constexpr int W = 4, NS = 4; };
-template <> struct KCfg<24> { static constexpr int W = 4, NS = 3; };
-template <> struct KCfg<32> { static constexpr int W = 4, NS = 3; };
-template <> struct KCfg<40> { static constexpr int W = 4, NS = 4; };
+// W warps per CTA, NS ring stages per warp (one 8-instance round each),
+// MINB CTAs per SM the register allocation must allow.
+template <> struct KCfg<16> { static constexpr int W = 4, NS = 2, MINB = 4; };
+template <> struct KCfg<24> { static constexpr int W = 2, NS = 2, MINB = 4; };
+template <> struct KCfg<32> { static constexpr int W = 2, NS = 2, MINB = 4; };
+template <> struct KCfg<40> { static constexpr int W = 2, NS = 2, MINB = 4; };
 
 template <int OUT>
 constexpr size_t smem_bytes() {
@@ -147,7 +170,7 @@ int sm_count(int dev) {
 template <int OUT, bool VARLEN>
 int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   constexpr int W = KCfg<OUT>::W, NS = KCfg<OUT>::NS;
-  auto kern = hash_kernel<OUT, VARLEN, W, NS>;
+  auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB>;
   const size_t smem = smem_bytes<OUT>();
   static std::once_flag once[64];
   int dev = 0;
@@ -189,15 +212,21 @@ int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
 }
 
 // fixed-mode geometry
+// warp job = one level-2 subtree (64 instances), or level-3 (512) for very
+// long strings so the per-job merge traffic and fences stay negligible
+int pick_job_lvl(u64 max_inst) { return max_inst >= (1ull << 15) ? 3 : 2; }
+
 struct FixedPlan {
   u64 n_inst, J, n_jobs, scr_per, cnt_per, ws_scratch, ws_acc, ws_cnt, ws_ev, ws_total;
+  int job_lvl;
 };
 FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
   FixedPlan f;
   f.n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
-  f.J = f.n_inst > (u64)JOB_INST ? ceil_div(f.n_inst, JOB_INST) : 1;
+  f.job_lvl = pick_job_lvl(f.n_inst);
+  f.J = job_count(f.n_inst, f.job_lvl);
   f.n_jobs = n_strings * f.J;
-  scratch_need(f.n_inst, v.k, &f.scr_per, &f.cnt_per);
+  scratch_need(f.n_inst, v.k, f.job_lvl, &f.scr_per, &f.cnt_per);
   const bool multi = f.J > 1;
   f.ws_scratch = align_up(n_strings * f.scr_per * 8, 256);
   f.ws_acc = multi ? align_up(n_strings * v.k * 8, 256) : 0;
@@ -214,7 +243,7 @@ struct VarPlan {
 };
 int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
   const u64 total_inst = total_bytes / (8ull * v.m);
-  p->max_jobs = n + total_inst / JOB_INST + 1;
+  p->max_jobs = n + total_inst / 64 + 1;
   p->scr_words = (total_inst / 56 + 1) * 8ull * v.k;
   p->cnts = total_inst / 448 + 1;
   size_t cub_bytes = 0;
@@ -292,11 +321,7 @@ int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_by
   return HTH_OK;
 }
 
-u64 fold_of(const uint8_t* m) {
-  u64 w[4];
-  memcpy(w, m, 32);
-  return w[0] ^ w[1] ^ w[2] ^ w[3];
-}
+
 
 }  // namespace
 
@@ -371,8 +396,8 @@ int hth_workspace_size_fixed(int output_bytes, uint64_t n_strings, uint64_t n_by
 }
 
 int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uint64_t stride_bytes, uint64_t n_bytes,
-                   const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out, void* d_workspace,
-                   uint64_t workspace_bytes, void* stream) {
+                   uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out,
+                   void* d_workspace, uint64_t workspace_bytes, void* stream) {
   VarInfo v;
   if (int rc = get_var(output_bytes, &v)) return rc;
   if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
@@ -397,6 +422,8 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.cnt_per = f.cnt_per;
   P.S = d_seed;
   P.out = d_out;
+  P.job_lvl = f.job_lvl;
+  fill_ehc(v, seed_fold, P);
   uint8_t* ws = (uint8_t*)d_workspace;
   P.scratch = (u64*)ws;
   P.acc = (u64*)(ws + f.ws_scratch);
@@ -416,8 +443,9 @@ int hth_workspace_size_varlen(int output_bytes, uint64_t n_strings, uint64_t tot
 }
 
 int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offsets, uint64_t n_strings,
-                    uint64_t max_n_bytes, uint64_t total_bytes, const uint64_t* d_seed, uint64_t seed_capacity,
-                    uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+                    uint64_t max_n_bytes, uint64_t total_bytes, uint64_t seed_fold, const uint64_t* d_seed,
+                    uint64_t seed_capacity, uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes,
+                    void* stream) {
   VarInfo v;
   if (int rc = get_var(output_bytes, &v)) return rc;
   if (int rc = check_seed(v, max_n_bytes, seed_capacity)) return rc;
@@ -440,11 +468,12 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   // plan areas of an earlier call may overlap this call's counters/accumulators
   CK(cudaMemsetAsync(ws + p.off_cnt, 0, p.off_cub - p.off_cnt, st));
   const u64 blocks = std::min<u64>(ceil_div(n_strings + 1, 256), 4096);
+  const int job_lvl = pick_job_lvl(((max_n_bytes + 7) / 8) / (u64)v.m);
   switch (output_bytes) {
-    case 16: plan_count_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
-    case 24: plan_count_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
-    case 32: plan_count_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
-    case 40: plan_count_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, tri, d_out, err); break;
+    case 16: plan_count_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
+    case 24: plan_count_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
+    case 32: plan_count_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
+    case 40: plan_count_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
   }
   CK(cudaGetLastError());
   size_t cub_bytes = p.cub_bytes;
@@ -461,6 +490,8 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_count)
   P.S = d_seed;
   P.out = d_out;
+  P.job_lvl = job_lvl;
+  fill_ehc(v, seed_fold, P);
   P.scratch = (u64*)(ws + p.off_scr);
   P.counters = (u32*)(ws + p.off_cnt);
   P.acc = (u64*)(ws + p.off_acc);
@@ -517,7 +548,7 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
     const u64 s0 = ch * per, ns = std::min(per, n_strings - s0);
     const uint8_t* src = (const uint8_t*)h_data + s0 * stride_bytes;
     if (n_bytes) CK(cudaMemcpyAsync(c->buf[b], src, (ns - 1) * stride_bytes + n_bytes, cudaMemcpyHostToDevice, st));
-    if (int rc = hth_hash_fixed(output_bytes, c->buf[b], ns, dstride, n_bytes, c->seeds, lay.total,
+    if (int rc = hth_hash_fixed(output_bytes, c->buf[b], ns, dstride, n_bytes, fold_of(master), c->seeds, lay.total,
                                 c->out + s0 * v.k, c->ws[b], c->ws_bytes, st))
       return rc;
     CK(cudaMemcpyAsync(h_out + s0 * v.k, c->out + s0 * v.k, ns * v.k * 8, cudaMemcpyDeviceToHost, st));

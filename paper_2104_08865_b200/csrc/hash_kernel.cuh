@@ -1,5 +1,5 @@
 // HalftimeHash B200 engine: the persistent warp-job hash kernel.
-// See engine.cuh for the decomposition; reference citations inline.
+// Decomposition and invariants: engine.cuh.  Reference citations inline.
 #pragma once
 #include "engine.cuh"
 
@@ -10,37 +10,126 @@ namespace hth {
 template <bool AL>
 __device__ __forceinline__ u64 ld_word(const uint8_t* buf, u32 delta, u32 widx) {
   if (AL) return *reinterpret_cast<const u64*>(buf + delta + widx * 8u);
-  u32 off = delta + widx * 8u;
+  const u32 off = delta + widx * 8u;
   const u64* p = reinterpret_cast<const u64*>(buf + (off & ~7u));
-  u32 sh = (off & 7u) * 8u;
+  const u32 sh = (off & 7u) * 8u;
   return (p[0] >> sh) | (p[1] << (64u - sh));
 }
 
-// Leaf of instance `q` of the stage, lane j -> C[r]   (hasher.py:356-364)
-template <class V, bool AL>
-__device__ __forceinline__ void stage_leaf(const uint8_t* buf, u32 delta, int q, int j, const u64* __restrict__ S,
-                                           u64 (&C)[V::k]) {
-  constexpr int M = Geo<V>::m;
-  w2 X[V::d][V::w];
-#pragma unroll
-  for (int i = 0; i < V::d; i++)
-#pragma unroll
-    for (int u = 0; u < V::w; u++) X[i][u] = mk(ld_word<AL>(buf, delta, (u32)(q * M + (i * V::w + u) * 8 + j)));
-  leaf<V>(X, S, C);
+template <int OUT>
+__device__ __forceinline__ void enc_planes(const u32 (&x)[4 * Var<OUT>::d], u32 (&y)[4 * (Var<OUT>::e - Var<OUT>::d)]) {
+  if constexpr (OUT == 24) enc_planes_24(x, y);
+  if constexpr (OUT == 32) enc_planes_32(x, y);
+  if constexpr (OUT == 40) enc_planes_40(x, y);
 }
 
-template <int K>
+template <int C>
+__device__ __forceinline__ u64 mac_sw(u64 acc, u64 h) {
+  return mac_const<C>(acc, h);
+}
+// acc += c * h for a coefficient c known after unrolling (params.py:17-27
+// shift/add forms; here two IMADs each)
+__device__ __forceinline__ u64 mac_coef(int c, u64 acc, u64 h) {
+  switch (c) {
+    case 1: return mac_sw<1>(acc, h);
+    case 2: return mac_sw<2>(acc, h);
+    case 3: return mac_sw<3>(acc, h);
+    case 4: return mac_sw<4>(acc, h);
+    case 5: return mac_sw<5>(acc, h);
+    case 7: return mac_sw<7>(acc, h);
+    case 8: return mac_sw<8>(acc, h);
+    case 9: return mac_sw<9>(acc, h);
+    default: return acc;
+  }
+}
+
+// EHC leaf of instances q and q+4 of the stage, lane j -> CA[r], CB[r]
+// (hasher.py:356-364; ehc.py:102-118).
+template <int OUT, bool AL>
+__device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int j, const Params& P,
+                                      u64 (&CA)[Var<OUT>::k], u64 (&CB)[Var<OUT>::k]) {
+  using V = Var<OUT>;
+  constexpr int K = V::k, E = V::e, D = V::d, WB = V::w, M = Geo<V>::m, NP = E - D;
+  u64 HA[E], HB[E];
+#pragma unroll
+  for (int i = 0; i < E; i++) HA[i] = HB[i] = 0;
+  const u32 offA = (u32)(q * M + j), offB = (u32)((q + 4) * M + j);
+#pragma unroll
+  for (int u = 0; u < WB; u++) {
+    w2 xa[D], xb[D];
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+      xa[i] = mk(ld_word<AL>(buf, delta, offA + (i * WB + u) * 8));
+      xb[i] = mk(ld_word<AL>(buf, delta, offB + (i * WB + u) * 8));
+    }
+    // hash the systematic items (ehc.py:49-72); seeds are constant-bank operands
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+      HA[i] = nh_acc(HA[i], xa[i], P.ehc_lo[i * WB + u], P.ehc_hi[i * WB + u]);
+      HB[i] = nh_acc(HB[i], xb[i], P.ehc_lo[i * WB + u], P.ehc_hi[i * WB + u]);
+    }
+    if constexpr (OUT == 16) {
+      // XOR parity code (params.py:105-112): one parity item = XOR of all inputs
+      w2 pa = xa[0], pb = xb[0];
+#pragma unroll
+      for (int i = 1; i < D; i++) {
+        pa = pa ^ xa[i];
+        pb = pb ^ xb[i];
+      }
+      HA[D] = nh_acc(HA[D], pa, P.ehc_lo[D * WB + u], P.ehc_hi[D * WB + u]);
+      HB[D] = nh_acc(HB[D], pb, P.ehc_lo[D * WB + u], P.ehc_hi[D * WB + u]);
+    } else {
+      // GF(16) Cauchy parity in bit-plane form: plane b of A | plane b of B << 16
+      u32 x[4 * D], y[4 * NP];
+#pragma unroll
+      for (int i = 0; i < D; i++) {
+        x[4 * i + 0] = __byte_perm(xa[i].lo, xb[i].lo, 0x5410);
+        x[4 * i + 1] = __byte_perm(xa[i].lo, xb[i].lo, 0x7632);
+        x[4 * i + 2] = __byte_perm(xa[i].hi, xb[i].hi, 0x5410);
+        x[4 * i + 3] = __byte_perm(xa[i].hi, xb[i].hi, 0x7632);
+      }
+      enc_planes<OUT>(x, y);
+#pragma unroll
+      for (int p = 0; p < NP; p++) {
+        const w2 pa = {__byte_perm(y[4 * p], y[4 * p + 1], 0x5410), __byte_perm(y[4 * p + 2], y[4 * p + 3], 0x5410)};
+        const w2 pb = {__byte_perm(y[4 * p], y[4 * p + 1], 0x7632), __byte_perm(y[4 * p + 2], y[4 * p + 3], 0x7632)};
+        HA[D + p] = nh_acc(HA[D + p], pa, P.ehc_lo[(D + p) * WB + u], P.ehc_hi[(D + p) * WB + u]);
+        HB[D + p] = nh_acc(HB[D + p], pb, P.ehc_lo[(D + p) * WB + u], P.ehc_hi[(D + p) * WB + u]);
+      }
+    }
+  }
+  // combine (ehc.py:75-99)
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    u64 a = 0, b = 0;
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      a = mac_coef(V::mat(r, i), a, HA[i]);
+      b = mac_coef(V::mat(r, i), b, HB[i]);
+    }
+    CA[r] = a;
+    CB[r] = b;
+  }
+}
+
+// Seed-region bases of a layout with L levels (hasher.py:130-153), computed
+// on demand rather than held in registers.
+template <int K, int EW>
 struct TreeCtx {
-  u64 T[K], F[K], R;
+  u32 L;
+  __device__ __forceinline__ u64 T(int r) const { return (u64)EW + 7ull * L * r; }
+  __device__ __forceinline__ u64 F(int r) const { return (u64)EW + 7ull * L * K + 64ull * L * r; }
+  __device__ __forceinline__ u64 R() const { return (u64)EW + 71ull * L * K; }
 };
 
-// A finished block at level `lvl` >= 2, index `idx` (lanes 0-7 hold lane j
-// of each row).  Either it is a leftover of its level -> finalize terms
-// (tree.py:103-134), or it joins a complete group of 8 whose node the last
-// arriving warp computes (nh.py:96-121 with level seeds, tree.py:55-60).
-template <int K>
-__device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeCtx<K>& tc, int lvl, u64 idx,
-                                      u64 (&B)[K], u64 (&fin)[K], int lane) {
+// A finished block at level `lvl` >= job_lvl, index `idx` (lanes 0-7 hold
+// lane j of each row).  Either it is a leftover of its level -> finalize
+// terms (tree.py:103-134), or it joins a complete group of 8 whose node the
+// last arriving warp computes (nh.py:96-121 with level seeds,
+// tree.py:55-60).  Returns the number of completion events (0 or 1).
+template <int K, int EW>
+__device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeCtx<K, EW>& tc, int lvl, u64 idx,
+                                     u64 (&B)[K], u64 (&fin)[K], int lane) {
   const int q = lane >> 3, j = lane & 7;
   const u64* __restrict__ S = P.S;
   for (;;) {
@@ -48,15 +137,15 @@ __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeC
     if (idx >= (len & ~7ull)) {
       if (lane < 8) {
 #pragma unroll
-        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B[r], __ldg(S + tc.F[r] + 56ull * lvl + (idx & 7) * 8 + j));
+        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B[r], __ldg(S + tc.F(r) + 56ull * lvl + (idx & 7) * 8 + j));
       }
       return 1;
     }
     u64 woff = 0, coff = 0;
-    for (int l = 2; l <= lvl; l++) {
+    for (int l = P.job_lvl; l <= lvl; l++) {
       const u64 ln = st.n_inst >> (3 * l);
       if (l < lvl) woff += (ln & ~7ull) * 8ull * K;
-      if (l >= 3) coff += ln;  // counters of levels 3..lvl precede level lvl+1's
+      if (l > P.job_lvl) coff += ln;  // counters of levels job_lvl+1..lvl precede level lvl+1's
     }
     u64* blk = P.scratch + st.scratch + woff;
     if (lane < 8) {
@@ -79,7 +168,7 @@ __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeC
       const u64 b = __ldcg(g + (q + 4) * 8 * K + r * 8 + j);
       g[q * 8 * K + r * 8 + j] = 0;  // consumed: leave the workspace zeroed
       g[(q + 4) * 8 * K + r * 8 + j] = 0;
-      const u64* s = S + tc.T[r] + 7ull * lvl;
+      const u64* s = S + tc.T(r) + 7ull * lvl;
       u64 v = nh_acc(0, a, __ldg(s + q));
       v = (q < 3) ? nh_acc(v, b, __ldg(s + q + 4)) : v + b;
       v += shfl_xor(v, 8);
@@ -91,8 +180,8 @@ __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeC
   }
 }
 
-template <int OUT, bool VARLEN, int W, int NS>
-__global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
+template <int OUT, bool VARLEN, int W, int NS, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constant__ Params P) {
   using V = Var<OUT>;
   constexpr int K = V::k, M = Geo<V>::m;
   constexpr u32 CB = ROUND_INST * M * 8;  // stage payload bytes
@@ -113,6 +202,7 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
   const u64 NW = (u64)gridDim.x * W;
   const u64 gw = (u64)blockIdx.x * W + warp;
   const u64 n_jobs = VARLEN ? P.meta[3 * P.n_strings] : P.n_jobs;
+  const int job_lvl = P.job_lvl;
   const u64* __restrict__ S = P.S;
   const u64 pol = policy_evict_first();
 
@@ -126,7 +216,7 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
     u32 jq, ni;
     u64 b0;
     decode_job<VARLEN, K, M>(P, pjob, st, jq);
-    job_span<M>(st, jq, b0, pbytes, ni);
+    job_span<M>(st, jq, job_lvl, b0, pbytes, ni);
     pbase = st.p + b0;
     pnchunks = (u32)ceil_div(pbytes, CB);
     pchunk = 0;
@@ -150,30 +240,43 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
     pchunk++;
   };
   if (pjob < n_jobs) p_load();
+#pragma unroll
   for (int s = 0; s < NS; s++) p_issue();
 
   // ---- consumer ----
   u32 cseq = 0;
+  u32 seedL = 0;                 // layout level count the cached tree seeds belong to
+  u64 s1A[K], s1B[K];            // level-1 node seeds of this thread's two positions
+  TreeCtx<K, Geo<V>::ew> tc;
+  tc.L = 0;
   for (u64 job = gw; job < n_jobs; job += NW) {
     Str st;
     u32 jq, ninst;
     u64 byte0, nbytes;
     decode_job<VARLEN, K, M>(P, job, st, jq);
-    job_span<M>(st, jq, byte0, nbytes, ninst);
+    job_span<M>(st, jq, job_lvl, byte0, nbytes, ninst);
     const u32 nchunks = (u32)ceil_div(nbytes, CB);
     const u32 delta = (u32)(reinterpret_cast<uintptr_t>(st.p) & 15);
     const bool last_job = (jq + 1 == st.J);
-    TreeCtx<K> tc;
-    layout_bases<K>(st.L, Geo<V>::ew, tc.T, tc.F, tc.R);
+    if (st.L != seedL) {
+      // tree seeds depend on the layout (hasher.py:130-153) via L only
+      tc.L = st.L;
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        s1A[r] = __ldg(S + tc.T(r) + q);
+        s1B[r] = q < 3 ? __ldg(S + tc.T(r) + q + 4) : 0;
+      }
+      seedL = st.L;
+    }
 
-    u64 fin[K], n1[K], n2[K];
+    u64 fin[K], n2[K], n3[K];
     u32 events = last_job ? 1u : 0u;
 #pragma unroll
-    for (int r = 0; r < K; r++) fin[r] = n1[r] = n2[r] = 0;
-    const u64 inst0 = (u64)jq * JOB_INST;
-    const u64 full0 = st.n_inst & ~7ull;      // level-0 blocks in complete groups
-    const u64 len1 = st.n_inst >> 3;          // level-1 blocks
-    const u64 full1 = len1 & ~7ull;
+    for (int r = 0; r < K; r++) fin[r] = n2[r] = n3[r] = 0;
+    const u64 inst0 = (u64)jq << (3 * job_lvl);
+    const u64 full0 = st.n_inst & ~7ull;  // instances in complete level-1 groups
+    const u64 len1 = st.n_inst >> 3, full1 = len1 & ~7ull;
+    const u64 len2 = st.n_inst >> 6, full2 = len2 & ~7ull;
 
     for (u32 c = 0; c < nchunks; c++) {
       const u32 slot = cseq % NS;
@@ -188,55 +291,71 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
         fence_proxy_async();
         __syncwarp();
       }
-      const u32 ri = c * ROUND_INST + q;
-      if (ri < ninst) {
-        u64 C[K];
+      const u32 r0 = c * ROUND_INST;  // first instance of the round (job-relative)
+      if (r0 < ninst) {
+        u64 CA[K], CB_[K];
         if (delta & 7)
-          stage_leaf<V, false>(buf, delta, q, j, S, C);
+          leaf2<OUT, false>(buf, delta, q, j, P, CA, CB_);
         else
-          stage_leaf<V, true>(buf, delta, q, j, S, C);
-        const u64 g = inst0 + ri;
-        const int pos = (int)(g & 7);
-        if (g < full0) {
-          // level-1 node term (nh_tree_node: last block added, not hashed)
-#pragma unroll
-          for (int r = 0; r < K; r++)
-            n1[r] = (pos < 7) ? nh_acc(n1[r], C[r], __ldg(S + tc.T[r] + pos)) : n1[r] + C[r];
-        } else {
-          // level-0 leftover -> finalize slot (0, pos)
-#pragma unroll
-          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], C[r], __ldg(S + tc.F[r] + pos * 8 + j));
-        }
-      }
-      if (c & 1) {
-        const u64 G1 = (inst0 >> 3) + (c >> 1);
+          leaf2<OUT, true>(buf, delta, q, j, P, CA, CB_);
+        const u64 G1 = (inst0 >> 3) + c;  // level-1 group of this round
         if (G1 < len1) {
+          // complete group -> level-1 node (nh_tree_node: last block added)
           u64 B1[K];
 #pragma unroll
           for (int r = 0; r < K; r++) {
-            u64 v = n1[r];
+            u64 v = nh_acc(0, CA[r], s1A[r]);
+            v = (q < 3) ? nh_acc(v, CB_[r], s1B[r]) : v + CB_[r];
             v += shfl_xor(v, 8);
             v += shfl_xor(v, 16);
             B1[r] = v;
-            n1[r] = 0;
           }
           const int p1 = (int)(G1 & 7);
           if (G1 >= full1) {
-            if (q == 0) {
+            if (q == 0) {  // level-1 leftover -> finalize slot (1, p1)
 #pragma unroll
-              for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B1[r], __ldg(S + tc.F[r] + 56 + p1 * 8 + j));
+              for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B1[r], __ldg(S + tc.F(r) + 56 + p1 * 8 + j));
             }
           } else {
             if (q == 0) {
 #pragma unroll
               for (int r = 0; r < K; r++)
-                n2[r] = (p1 < 7) ? nh_acc(n2[r], B1[r], __ldg(S + tc.T[r] + 7 + p1)) : n2[r] + B1[r];
+                n2[r] = (p1 < 7) ? nh_acc(n2[r], B1[r], __ldg(S + tc.T(r) + 7 + p1)) : n2[r] + B1[r];
             }
             if (p1 == 7) {
-              events += climb<K>(P, st, tc, 2, G1 >> 3, n2, fin, lane);
+              const u64 G2 = G1 >> 3;  // level-2 block complete in lanes 0-7
+              if (job_lvl == 2) {
+                events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, n2, fin, lane);
+              } else {
+                const int p2 = (int)(G2 & 7);
+                if (lane < 8) {
+                  if (G2 >= full2) {
+#pragma unroll
+                    for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], n2[r], __ldg(S + tc.F(r) + 112 + p2 * 8 + j));
+                  } else {
+#pragma unroll
+                    for (int r = 0; r < K; r++)
+                      n3[r] = (p2 < 7) ? nh_acc(n3[r], n2[r], __ldg(S + tc.T(r) + 14 + p2)) : n3[r] + n2[r];
+                  }
+                }
+                if (G2 < full2 && p2 == 7) {
+                  events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, n3, fin, lane);
+#pragma unroll
+                  for (int r = 0; r < K; r++) n3[r] = 0;
+                }
+              }
 #pragma unroll
               for (int r = 0; r < K; r++) n2[r] = 0;
             }
+          }
+        } else {
+          // incomplete last group: level-0 leftovers -> finalize slot (0, pos)
+          const u64 gA = inst0 + r0 + q, gB = gA + 4;
+          const bool vA = r0 + q < ninst, vB = r0 + q + 4 < ninst;
+#pragma unroll
+          for (int r = 0; r < K; r++) {
+            if (vA) fin[r] = nh_acc(fin[r], CA[r], __ldg(S + tc.F(r) + (gA & 7) * 8 + j));
+            if (vB) fin[r] = nh_acc(fin[r], CB_[r], __ldg(S + tc.F(r) + (gB & 7) * 8 + j));
           }
         }
       }
@@ -249,7 +368,7 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
         for (u32 t = lane; t < nt; t += 32) {
           const u64 y = (delta & 7) ? ld_word<false>(buf, delta, cw0 + t) : ld_word<true>(buf, delta, cw0 + t);
 #pragma unroll
-          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], y, __ldg(S + tc.R + r + t));
+          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], y, __ldg(S + tc.R() + r + t));
         }
       }
       __syncwarp();
@@ -265,16 +384,16 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
           const u32 l = x / 56u, slot = (x % 56u) >> 3;
           if (slot >= (u32)((st.n_inst >> (3 * l)) & 7)) {
 #pragma unroll
-            for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], 0ull, __ldg(S + tc.F[r] + x));
+            for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], 0ull, __ldg(S + tc.F(r) + x));
           }
         }
         if (lane == 0) {
 #pragma unroll
-          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, __ldg(S + tc.F[r] + nz));
+          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, __ldg(S + tc.F(r) + nz));
         }
       } else if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, __ldg(S + tc.F[r]));
+        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, __ldg(S + tc.F(r)));
       }
     }
     u64 mine = 0;
@@ -296,7 +415,7 @@ __global__ void __launch_bounds__(W * 32) hash_kernel(const Params P) {
       u32 old = 0;
       if (lane == 0) old = atomicAdd(P.events + st.s, events);
       old = __shfl_sync(0xffffffffu, old, 0);
-      if (old + events == string_events(st.n_inst)) {
+      if (old + events == string_events(st.n_inst, job_lvl)) {
         __threadfence();
         if (lane < K) P.out[st.s * K + lane] = atomicExch(a + lane, 0ull);
         if (lane == 0) P.events[st.s] = 0;
