@@ -11,6 +11,7 @@
 
 #include "../../include/halftime_b200.h"
 #include "hash_kernel.cuh"
+#include "tail_kernel.cuh"
 
 using namespace hth;
 
@@ -189,6 +190,36 @@ int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   kern<<<(unsigned)grid, W * 32, smem, st>>>(P);
   CK(cudaGetLastError());
   return HTH_OK;
+}
+
+template <int OUT, int CPT>
+int launch_tail(const TailParams& P, cudaStream_t st) {
+  auto kern = tail_kernel<OUT, CPT>;
+  static int occ[64] = {0};
+  static std::once_flag once[64];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [&]() {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, 0);
+    occ[dev & 63] = o > 0 ? o : 1;
+  });
+  const u64 pairs = (P.n_strings + 1) / 2;
+  u64 grid = (u64)sm_count(dev) * occ[dev & 63];
+  const u64 need = ceil_div(pairs, 8);
+  if (need < grid) grid = need;
+  kern<<<(unsigned)std::max<u64>(grid, 1), 256, 0, st>>>(P);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+
+template <int OUT>
+int dispatch_tail(const TailParams& P, u64 nch, cudaStream_t st) {
+  const u64 cpt = ceil_div(nch, 16);
+  if (cpt <= 1) return launch_tail<OUT, 1>(P, st);
+  if (cpt <= 2) return launch_tail<OUT, 2>(P, st);
+  if (cpt <= 4) return launch_tail<OUT, 4>(P, st);
+  return launch_tail<OUT, 6>(P, st);
 }
 
 template <bool VARLEN>
@@ -424,6 +455,29 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.out = d_out;
   P.job_lvl = f.job_lvl;
   fill_ehc(v, seed_fold, P);
+  if (f.n_inst == 0 && stride_bytes % 16 == 0) {
+    // strings shorter than one instance: dedicated half-warp-per-string kernel
+    TailParams T{};
+    T.data = (const uint8_t*)d_data;
+    T.n_strings = n_strings;
+    T.stride = stride_bytes;
+    T.n_bytes = n_bytes;
+    T.S = d_seed;
+    T.R = (u64)v.ew + 71ull * v.k;
+    T.out = d_out;
+    for (int r = 0; r < v.k; r++) {  // finalize over the tag alone (hasher.py:400-405)
+      const u64 sF = host_mix(seed_fold + ((u64)v.ew + 7ull * v.k + 64ull * r + 1) * 0x9E3779B97F4A7C15ull);
+      const u32 a = (u32)n_bytes + (u32)sF, b = (u32)(n_bytes >> 32) + (u32)(sF >> 32);
+      T.tag[r] = (u64)a * b;
+    }
+    const u64 nch = (n_bytes + 15) / 16;
+    switch (output_bytes) {
+      case 16: return dispatch_tail<16>(T, nch, st);
+      case 24: return dispatch_tail<24>(T, nch, st);
+      case 32: return dispatch_tail<32>(T, nch, st);
+      case 40: return dispatch_tail<40>(T, nch, st);
+    }
+  }
   uint8_t* ws = (uint8_t*)d_workspace;
   P.scratch = (u64*)ws;
   P.acc = (u64*)(ws + f.ws_scratch);

@@ -98,6 +98,17 @@ def test_every_short_length(hh, w):
 
 
 @pytest.mark.parametrize("w", VARIANTS)
+def test_tail_only_kernel(hh, w):
+    # strings shorter than one instance with 16-byte-aligned strides take the
+    # dedicated tail kernel (hth_hash_fixed dispatch); odd batch sizes too
+    v = o.variant(w)
+    iw = v.m * 8
+    for n in list(range(0, 130)) + [255, 256, 257, 1000, 1023, 1024, iw - 17, iw - 9, iw - 8, iw - 1]:
+        stride = (n + 15) // 16 * 16
+        _check_fixed(hh, w, 37, n, stride=max(stride, 16))
+
+
+@pytest.mark.parametrize("w", VARIANTS)
 def test_multi_job_and_tree_levels(hh, w):
     # job boundaries (64 instances), level-2 / level-3 merges, powers of 8 +- 1
     v = o.variant(w)
