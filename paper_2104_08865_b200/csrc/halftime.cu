@@ -192,34 +192,39 @@ int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   return HTH_OK;
 }
 
-template <int OUT, int CPT>
+template <int OUT, int CPT, bool MASKED>
 int launch_tail(const TailParams& P, cudaStream_t st) {
-  auto kern = tail_kernel<OUT, CPT>;
-  static int occ[64] = {0};
-  static std::once_flag once[64];
+  constexpr int NS = 4, TPB = 256;
+  auto kern = tail_kernel<OUT, CPT, MASKED, NS>;
+  const u64 sby = (2 * P.stride + 127) & ~127ull;
+  const size_t smem = (TPB / 32) * NS * (sby + 8);
+  if (smem > 227 * 1024) return fail(HTH_EINVAL, "tail kernel stage too large");
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  std::call_once(once[dev & 63], [&]() {
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, 0);
-    occ[dev & 63] = o > 0 ? o : 1;
-  });
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, smem));
   const u64 pairs = (P.n_strings + 1) / 2;
-  u64 grid = (u64)sm_count(dev) * occ[dev & 63];
-  const u64 need = ceil_div(pairs, 8);
+  u64 grid = (u64)sm_count(dev) * std::max(occ, 1);
+  const u64 need = ceil_div(pairs, TPB / 32);
   if (need < grid) grid = need;
-  kern<<<(unsigned)std::max<u64>(grid, 1), 256, 0, st>>>(P);
+  kern<<<(unsigned)std::max<u64>(grid, 1), TPB, smem, st>>>(P);
   CK(cudaGetLastError());
   return HTH_OK;
 }
 
+template <int OUT, bool MASKED>
+int dispatch_tail_m(const TailParams& P, u64 nch, cudaStream_t st) {
+  const u64 cpt = ceil_div(nch, 16);
+  if (cpt <= 1) return launch_tail<OUT, 1, MASKED>(P, st);
+  if (cpt <= 2) return launch_tail<OUT, 2, MASKED>(P, st);
+  if (cpt <= 4) return launch_tail<OUT, 4, MASKED>(P, st);
+  return launch_tail<OUT, 6, MASKED>(P, st);
+}
 template <int OUT>
 int dispatch_tail(const TailParams& P, u64 nch, cudaStream_t st) {
-  const u64 cpt = ceil_div(nch, 16);
-  if (cpt <= 1) return launch_tail<OUT, 1>(P, st);
-  if (cpt <= 2) return launch_tail<OUT, 2>(P, st);
-  if (cpt <= 4) return launch_tail<OUT, 4>(P, st);
-  return launch_tail<OUT, 6>(P, st);
+  const bool masked = (P.n_bytes % 16) != 0 || (nch % 16) != 0;
+  return masked ? dispatch_tail_m<OUT, true>(P, nch, st) : dispatch_tail_m<OUT, false>(P, nch, st);
 }
 
 template <bool VARLEN>
@@ -455,7 +460,7 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.out = d_out;
   P.job_lvl = f.job_lvl;
   fill_ehc(v, seed_fold, P);
-  if (f.n_inst == 0 && stride_bytes % 16 == 0) {
+  if (f.n_inst == 0 && n_bytes > 0 && stride_bytes % 16 == 0 && stride_bytes <= 2048) {
     // strings shorter than one instance: dedicated half-warp-per-string kernel
     TailParams T{};
     T.data = (const uint8_t*)d_data;

@@ -5,7 +5,7 @@
 // (hasher.py:400-412: finalize over the tag only, plus the Toeplitz tail).
 //
 // A half-warp hashes one string: lane g owns the 16-byte chunks g, g+16, ...
-// (coalesced 128-bit loads, 256 contiguous bytes per half-warp per load).
+// staged through a per-warp cp.async.bulk ring (128-bit shared loads).
 // The Toeplitz key words a lane needs are the same for every string, so they
 // are loaded once into registers; the tag term is a launch constant computed
 // on the host.  Per string the lanes' k partial sums are combined with a
@@ -26,14 +26,6 @@ struct TailParams {
   u64* out;
   u64 tag[5];  // NH(n, S[F_r]) per output word
 };
-
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
 
 // Sum v[0..K) over the 16 lanes of each half-warp; afterwards lane g holds
 // the total of word (g & (KP-1)) for g < KP (KP = K rounded up to 2^n).
@@ -79,17 +71,32 @@ __device__ __forceinline__ int scatter_index(int g) {
   return idx;
 }
 
-template <int OUT, int CPT>
+// Per warp: a ring of NS stages, each one cp.async.bulk copy of a PAIR of
+// consecutive strings (2 x stride bytes), so the loads stay deep in flight
+// without holding registers.  MASKED: n % 16 != 0 (partial words / chunks).
+template <int OUT, int CPT, bool MASKED, int NS>
 __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ TailParams P) {
   constexpr int K = Var<OUT>::k;
-  const int lane = threadIdx.x & 31, g = lane & 15, half = lane >> 4;
+  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane & 15, half = lane >> 4;
   const u64 n = P.n_bytes;
   const u32 nw = (u32)((n + 7) >> 3);
   const u32 nch = (u32)((n + 15) >> 4);
+  const u32 stage_bytes = (u32)(2 * P.stride);
+  const u32 SBY = (stage_bytes + 127) & ~127u;
+  uint8_t* ring = smem + (size_t)warp * NS * SBY;
+  u64* bars = reinterpret_cast<u64*>(smem + (size_t)(blockDim.x >> 5) * NS * SBY) + warp * NS;
+  if (lane == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    fence_proxy_async();
+  }
+  __syncwarp();
   // Toeplitz keys for this lane's chunks: chunk c covers words 2c, 2c+1 and
   // needs S[R + 2c + r] for r <= K
   u32 klo[CPT][K + 1], khi[CPT][K + 1];
-  u64 mask0[CPT], mask1[CPT];  // zero-padding / words past the end
+  u64 mask0[CPT], mask1[CPT];  // zero-padding / words past the end (MASKED only)
 #pragma unroll
   for (int i = 0; i < CPT; i++) {
     const u32 c = (u32)g + 16u * i;
@@ -103,47 +110,67 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
     mask0[i] = b0 >= n ? 0 : (b0 + 8 <= n ? ~0ull : (1ull << (8 * (n - b0))) - 1);
     mask1[i] = b1 >= n ? 0 : (b1 + 8 <= n ? ~0ull : (1ull << (8 * (n - b1))) - 1);
   }
-  const u64 warps = (u64)gridDim.x * (blockDim.x >> 5);
-  const u64 w0 = (u64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const u64 NW = (u64)gridDim.x * (blockDim.x >> 5);
+  const u64 w0 = (u64)blockIdx.x * (blockDim.x >> 5) + warp;
   const u64 pairs = (P.n_strings + 1) >> 1;
   const int myidx = scatter_index<K>(g);
+  const u64 pol = policy_evict_first();
+  const u64 total_bytes = (P.n_strings - 1) * P.stride + ((n + 15) & ~15ull);
 
-  uint4 cur[CPT], nxt[CPT];
-  auto load = [&](u64 pr, uint4 (&dst)[CPT]) {
-    const u64 s = 2 * pr + half;
-    const uint8_t* base = P.data + s * P.stride;
+  u64 pnext = w0;
+  u32 pseq = 0;
+  auto issue = [&]() {
+    if (pnext >= pairs) return;
+    const u64 off = 2 * pnext * P.stride;
+    const u32 bytes = (u32)min((u64)stage_bytes, total_bytes - off);
+    const u32 slot = pseq % NS;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[slot], bytes);
+      bulk_g2s(ring + slot * SBY, P.data + off, bytes, &bars[slot], pol);
+    }
+    pseq++;
+    pnext += NW;
+  };
+#pragma unroll
+  for (int s = 0; s < NS; s++) issue();
+
+  u32 cseq = 0;
+  for (u64 pr = w0; pr < pairs; pr += NW) {
+    const u32 slot = cseq % NS;
+    mbar_wait(&bars[slot], (cseq / NS) & 1);
+    const uint8_t* sb = ring + slot * SBY + (u32)half * (u32)P.stride;
+    uint4 v[CPT];
 #pragma unroll
     for (int i = 0; i < CPT; i++) {
       const u32 c = (u32)g + 16u * i;
-      dst[i] = (s < P.n_strings && c < nch) ? ldg_stream(base + 16ull * c) : make_uint4(0, 0, 0, 0);
+      v[i] = (!MASKED || c < nch) ? *reinterpret_cast<const uint4*>(sb + 16u * c) : make_uint4(0, 0, 0, 0);
     }
-  };
-  if (w0 < pairs) load(w0, cur);
-  for (u64 pr = w0; pr < pairs; pr += warps) {
-    if (pr + warps < pairs) load(pr + warps, nxt);
+    __syncwarp();
+    cseq++;
+    issue();  // refill the slot just read
     u64 acc[K];
 #pragma unroll
     for (int r = 0; r < K; r++) acc[r] = 0;
 #pragma unroll
     for (int i = 0; i < CPT; i++) {
       const u32 c = (u32)g + 16u * i;
-      if (c < nch) {
-        const u64 x0 = (((u64)cur[i].y << 32) | cur[i].x) & mask0[i];
-        const u64 x1 = (((u64)cur[i].w << 32) | cur[i].z) & mask1[i];
-        const bool w1 = 2 * c + 1 < nw;
+      if (!MASKED || c < nch) {
+        w2 x0 = {v[i].x, v[i].y}, x1 = {v[i].z, v[i].w};
+        if (MASKED) {
+          x0 = mk((((u64)v[i].y << 32) | v[i].x) & mask0[i]);
+          x1 = mk((((u64)v[i].w << 32) | v[i].z) & mask1[i]);
+        }
+        const bool w1 = !MASKED || 2 * c + 1 < nw;
 #pragma unroll
         for (int r = 0; r < K; r++) {
-          acc[r] = nh_acc(acc[r], mk(x0), klo[i][r], khi[i][r]);
-          if (w1) acc[r] = nh_acc(acc[r], mk(x1), klo[i][r + 1], khi[i][r + 1]);
+          acc[r] = nh_acc(acc[r], x0, klo[i][r], khi[i][r]);
+          if (w1) acc[r] = nh_acc(acc[r], x1, klo[i][r + 1], khi[i][r + 1]);
         }
       }
     }
     const u64 tot = half_reduce_scatter<K>(acc, g);
     const u64 s = 2 * pr + half;
-    constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
     if ((g & (16 / KP - 1)) == 0 && myidx < K && s < P.n_strings) P.out[s * K + myidx] = tot + P.tag[myidx];
-#pragma unroll
-    for (int i = 0; i < CPT; i++) cur[i] = nxt[i];
   }
 }
 
