@@ -119,6 +119,16 @@ __device__ __forceinline__ w2 xtime(w2 v) {
   return {nlo, nhi};
 }
 
+// Arrival on a merge/completion counter: release publishes this warp's
+// prior stores (ordered before lane 0 by __syncwarp), acquire makes the
+// other warps' blocks visible to a last arriver.  Lowers to MEMBAR.ALL.GPU
+// + ATOMG + CCTL.IVALL, cheaper than __threadfence()'s MEMBAR.SC.
+__device__ __forceinline__ u32 atom_add_acq_rel(u32* p, u32 v) {
+  u32 old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 template <class T>
 __device__ __forceinline__ T shfl_xor(T v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
@@ -200,7 +210,8 @@ struct Params {
   int job_lvl;    // a warp job is one level-`job_lvl` subtree
   // EHC seed words S[0..e*w), split into halves.  The kernel takes Params as
   // a __grid_constant__, so these are constant-bank operands of the NH adds.
-  u32 ehc_lo[MAX_EW], ehc_hi[MAX_EW];
+  // Interleaved (lo, hi) so one 64-bit constant load fetches both halves.
+  alignas(8) u32 ehc[2 * MAX_EW];
 };
 
 template <int K>
@@ -226,8 +237,10 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u3
     st.scratch = mt[1];
     st.cnt = mt[2];
   } else {
-    s = job / P.J_fixed;
-    jq = (u32)(job - s * P.J_fixed);
+    // jq-major order: all strings' first jobs, then all second jobs, ...
+    // Jobs of one jq have equal size, so static round-robin stays balanced.
+    jq = (u32)(job / P.n_strings);
+    s = job - (u64)jq * P.n_strings;
     st.p = P.data + s * P.stride;
     st.n = P.n_bytes;
     st.scratch = s * P.scr_per;

@@ -73,8 +73,8 @@ u64 host_mix(u64 z) {
 void fill_ehc(const VarInfo& v, u64 fold, Params& P) {
   for (int i = 0; i < v.ew; i++) {
     const u64 w = host_mix(fold + (u64)(i + 1) * 0x9E3779B97F4A7C15ull);
-    P.ehc_lo[i] = (u32)w;
-    P.ehc_hi[i] = (u32)(w >> 32);
+    P.ehc[2 * i] = (u32)w;
+    P.ehc[2 * i + 1] = (u32)(w >> 32);
   }
 }
 
@@ -250,7 +250,7 @@ int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
 // fixed-mode geometry
 // warp job = one level-2 subtree (64 instances), or level-3 (512) for very
 // long strings so the per-job merge traffic and fences stay negligible
-int pick_job_lvl(u64 max_inst) { return max_inst >= (1ull << 15) ? 3 : 2; }
+int pick_job_lvl(u64 max_inst) { return max_inst >= 512 ? 3 : 2; }
 
 struct FixedPlan {
   u64 n_inst, J, n_jobs, scr_per, cnt_per, ws_scratch, ws_acc, ws_cnt, ws_ev, ws_total;

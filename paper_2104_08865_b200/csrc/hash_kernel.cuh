@@ -65,8 +65,8 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
     // hash the systematic items (ehc.py:49-72); seeds are constant-bank operands
 #pragma unroll
     for (int i = 0; i < D; i++) {
-      HA[i] = nh_acc(HA[i], xa[i], P.ehc_lo[i * WB + u], P.ehc_hi[i * WB + u]);
-      HB[i] = nh_acc(HB[i], xb[i], P.ehc_lo[i * WB + u], P.ehc_hi[i * WB + u]);
+      HA[i] = nh_acc(HA[i], xa[i], P.ehc[2 * (i * WB + u)], P.ehc[2 * (i * WB + u) + 1]);
+      HB[i] = nh_acc(HB[i], xb[i], P.ehc[2 * (i * WB + u)], P.ehc[2 * (i * WB + u) + 1]);
     }
     if constexpr (OUT == 16) {
       // XOR parity code (params.py:105-112): one parity item = XOR of all inputs
@@ -76,8 +76,8 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
         pa = pa ^ xa[i];
         pb = pb ^ xb[i];
       }
-      HA[D] = nh_acc(HA[D], pa, P.ehc_lo[D * WB + u], P.ehc_hi[D * WB + u]);
-      HB[D] = nh_acc(HB[D], pb, P.ehc_lo[D * WB + u], P.ehc_hi[D * WB + u]);
+      HA[D] = nh_acc(HA[D], pa, P.ehc[2 * (D * WB + u)], P.ehc[2 * (D * WB + u) + 1]);
+      HB[D] = nh_acc(HB[D], pb, P.ehc[2 * (D * WB + u)], P.ehc[2 * (D * WB + u) + 1]);
     } else {
       // GF(16) Cauchy parity in bit-plane form: plane b of A | plane b of B << 16
       u32 x[4 * D], y[4 * NP];
@@ -93,8 +93,8 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
       for (int p = 0; p < NP; p++) {
         const w2 pa = {__byte_perm(y[4 * p], y[4 * p + 1], 0x5410), __byte_perm(y[4 * p + 2], y[4 * p + 3], 0x5410)};
         const w2 pb = {__byte_perm(y[4 * p], y[4 * p + 1], 0x7632), __byte_perm(y[4 * p + 2], y[4 * p + 3], 0x7632)};
-        HA[D + p] = nh_acc(HA[D + p], pa, P.ehc_lo[(D + p) * WB + u], P.ehc_hi[(D + p) * WB + u]);
-        HB[D + p] = nh_acc(HB[D + p], pb, P.ehc_lo[(D + p) * WB + u], P.ehc_hi[(D + p) * WB + u]);
+        HA[D + p] = nh_acc(HA[D + p], pa, P.ehc[2 * ((D + p) * WB + u)], P.ehc[2 * ((D + p) * WB + u) + 1]);
+        HB[D + p] = nh_acc(HB[D + p], pb, P.ehc[2 * ((D + p) * WB + u)], P.ehc[2 * ((D + p) * WB + u) + 1]);
       }
     }
   }
@@ -152,14 +152,12 @@ __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeC
 #pragma unroll
       for (int r = 0; r < K; r++) blk[idx * 8 * K + r * 8 + j] = B[r];
     }
-    __threadfence();
     __syncwarp();
     u32 old = 0;
     u32* ctr = P.counters + st.cnt + coff + (idx >> 3);
-    if (lane == 0) old = atomicAdd(ctr, 1u);
+    if (lane == 0) old = atom_add_acq_rel(ctr, 1u);
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != 7) return 0;
-    __threadfence();
     if (lane == 0) *ctr = 0;  // last arriver: leave the workspace zeroed
     u64* g = blk + (idx & ~7ull) * 8 * K;
 #pragma unroll
@@ -410,13 +408,11 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       // re-zeroes the accumulators (integer sums: order-independent).
       unsigned long long* a = reinterpret_cast<unsigned long long*>(P.acc + st.s * K);
       if (lane < K) atomicAdd(a + lane, (unsigned long long)mine);
-      __threadfence();
       __syncwarp();
       u32 old = 0;
-      if (lane == 0) old = atomicAdd(P.events + st.s, events);
+      if (lane == 0) old = atom_add_acq_rel(P.events + st.s, events);
       old = __shfl_sync(0xffffffffu, old, 0);
       if (old + events == string_events(st.n_inst, job_lvl)) {
-        __threadfence();
         if (lane < K) P.out[st.s * K + lane] = atomicExch(a + lane, 0ull);
         if (lane == 0) P.events[st.s] = 0;
       }
