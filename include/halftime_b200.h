@@ -112,6 +112,32 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
  * workspace met a string longer than its max_n_bytes, else HTH_OK. */
 int hth_varlen_status(void* d_workspace, void* stream);
 
+/* ---- one string split across devices (config 5): the reference's stack
+ * construction is front-aligned (tree.py:63-100), so a string cut at
+ * multiples of 8^c instances splits into independent level-c subtrees.
+ * hth_slice_plan: instance bounds of n_slices balanced slices (the last one
+ * also takes the ragged end and the tail), the frontier level c, and how
+ * many level-c subtree roots each slice emits.
+ * hth_hash_slice: hash instances [inst_begin, inst_end) of a string of
+ * n_bytes; d_slice holds its bytes from inst_begin*m*8 up to inst_end*m*8 (or
+ * to n_bytes for the last slice).  Writes the slice's frontier (count from
+ * the plan, k*8 u64 per root) and zeroes then fills d_partial (k words).
+ * Workspace: hth_workspace_size_slice, zero-filled like hth_hash_fixed's.
+ * hth_hash_merge: given all slices' frontiers concatenated in slice order and
+ * their partials, finishes the tree and writes the k digest words.
+ * Workspace: >= 16*k*(n_frontier/8 + 8)*8 bytes. */
+int hth_slice_plan(int output_bytes, uint64_t n_bytes, uint64_t n_slices, uint64_t* inst_bounds, int* frontier_level,
+                   uint64_t* frontier_counts);
+int hth_workspace_size_slice(int output_bytes, uint64_t n_bytes, uint64_t* bytes);
+int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
+                   int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
+                   uint64_t* d_frontier, uint64_t* d_partial, void* d_workspace, uint64_t workspace_bytes,
+                   void* stream);
+int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
+                   uint64_t n_frontier, const uint64_t* d_partials, uint64_t n_partials, uint64_t seed_fold,
+                   const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out, void* d_workspace,
+                   uint64_t workspace_bytes, void* stream);
+
 /* ---- host-buffer entry points (end-to-end; synchronous).  These are what
  * hash_bytes(..., engine="cuda") binds: host bytes in, host digest words
  * out, seeds expanded on the device from the 32-byte master.  The batch

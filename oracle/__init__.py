@@ -52,7 +52,9 @@ def lib():
         L.hto_hash_fixed.argtypes = [i32, vp, u64, u64, u64, vp, u64, vp, i32]
         L.hto_hash_varlen.argtypes = [i32, vp, vp, u64, vp, u64, vp, i32]
         L.hto_hash_huge.argtypes = [i32, vp, u64, vp, u64, vp, i32]
-        for f in (L.hto_hash_one, L.hto_hash_fixed, L.hto_hash_varlen, L.hto_hash_huge):
+        L.hto_slice.argtypes = [i32, vp, u64, u64, u64, i32, vp, u64, vp, vp]
+        L.hto_merge.argtypes = [i32, u64, i32, vp, u64, vp, u64, vp, u64, vp]
+        for f in (L.hto_hash_one, L.hto_hash_fixed, L.hto_hash_varlen, L.hto_hash_huge, L.hto_slice, L.hto_merge):
             f.restype = i32
         _LIB = L
     return _LIB
@@ -123,3 +125,25 @@ class c:
         cls._rc(lib().hto_hash_huge(out_bytes, _ptr(data), data.nbytes, _ptr(seeds), seeds.size,
                                     _ptr(out), _threads(threads)))
         return out
+
+    @classmethod
+    def slice(cls, out_bytes, data: np.ndarray, n_bytes, inst_begin, inst_end, level, count, seeds):
+        """Frontier (count, k*8) and partial (k,) of one slice; `data` is the whole string."""
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        k = cls._k(out_bytes)
+        fr = np.zeros((max(count, 1), k * 8), dtype=np.uint64)
+        part = np.zeros(k, dtype=np.uint64)
+        cls._rc(lib().hto_slice(out_bytes, _ptr(data), n_bytes, inst_begin, inst_end, level, _ptr(seeds),
+                                seeds.size, _ptr(fr), _ptr(part)))
+        return fr[:count], part
+
+    @classmethod
+    def merge(cls, out_bytes, n_bytes, level, frontier: np.ndarray, partials: np.ndarray, seeds):
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        fr = np.ascontiguousarray(frontier, dtype=np.uint64)
+        pa = np.ascontiguousarray(partials, dtype=np.uint64)
+        out = np.zeros(cls._k(out_bytes), dtype=np.uint64)
+        cls._rc(lib().hto_merge(out_bytes, n_bytes, level, _ptr(fr), fr.shape[0], _ptr(pa), pa.shape[0],
+                                _ptr(seeds), seeds.size, _ptr(out)))
+        return out
+

@@ -302,3 +302,103 @@ int hto_hash_huge(int out_bytes, const uint8_t* p, uint64_t n, const uint64_t* S
     free(st); free(roots);
     return 0;
 }
+
+/*
+ * Slice / merge restatement of the same hash, for checking the multi-device
+ * decomposition (test infrastructure).  A string cut at multiples of 8^c
+ * instances splits into independent level-c subtrees because the stack
+ * construction groups blocks front-aligned (tree.py:63-100).  The finalize
+ * NH (tree.py:103-134) and the tail (hasher.py:186-206) are sums of terms,
+ * so each slice contributes a partial sum; level-c roots that are not
+ * leftovers ("frontier") are finished by the merge.
+ */
+static uint64_t fin_term(const hto_variant* v, const hto_layout* lay, const uint64_t* S, int r, int lvl,
+                         uint64_t slot, const uint64_t blk[8]) {
+    uint64_t acc = 0;
+    for (int j = 0; j < 8; j++) acc += nh(blk[j], S[lay->F[r] + 56ull * lvl + slot * 8 + j]);
+    (void)v;
+    return acc;
+}
+
+int hto_slice(int out_bytes, const uint8_t* p, uint64_t n, uint64_t a, uint64_t b, int c, const uint64_t* S,
+              uint64_t cap, uint64_t* frontier, uint64_t* partial) {
+    hto_variant v; hto_layout lay;
+    int rc = check(out_bytes, n, cap, &v, &lay);
+    if (rc) return rc;
+    for (int r = 0; r < v.k; r++) partial[r] = 0;
+    const uint64_t keep = (lay.n_inst >> (3 * c)) & ~7ull, fbase = a >> (3 * c);
+    stack_t_* st = (stack_t_*)calloc(1, sizeof *st);
+    uint64_t C[5][8];
+    for (uint64_t t = a; t < b; t++) {
+        leaf(&v, p, n, t, S, C);
+        push(&v, st, 0, C, &lay, S);
+        if (st->cnt[c] == 1) {  /* a level-c root just completed */
+            uint64_t idx = t >> (3 * c);
+            if (idx < keep) {
+                for (int r = 0; r < v.k; r++) memcpy(frontier + (idx - fbase) * 8 * v.k + r * 8, st->blk[c][0][r], 64);
+            } else {
+                for (int r = 0; r < v.k; r++) partial[r] += fin_term(&v, &lay, S, r, c, idx & 7, st->blk[c][0][r]);
+            }
+            st->cnt[c] = 0;
+        }
+    }
+    if (b == lay.n_inst) {  /* last slice: leftovers below c, every zero slot, tag, tail */
+        for (int r = 0; r < v.k; r++) {
+            uint64_t acc = 0;
+            if (lay.n_inst) {
+                const uint64_t* s = S + lay.F[r];
+                for (int l = 0; l < lay.L; l++) {
+                    const int digit = (int)((lay.n_inst >> (3 * l)) & 7);
+                    for (int q = 0; q < 7; q++)
+                        for (int j = 0; j < 8; j++) {
+                            if (q >= digit) acc += nh(0, s[l * 56 + q * 8 + j]);             /* zero slot */
+                            else if (l < c) acc += nh(st->blk[l][q][r][j], s[l * 56 + q * 8 + j]);
+                        }
+                }
+                acc += nh(n, s[lay.L * 56]);
+            } else {
+                acc += nh(n, S[lay.F[r]]);
+            }
+            uint64_t nw = (n + 7) / 8, t0 = lay.n_inst * v.m;
+            for (uint64_t t = t0; t < nw; t++) acc += nh(load_word(p, n, t), S[lay.R + r + (t - t0)]);
+            partial[r] += acc;
+        }
+    }
+    free(st);
+    return 0;
+}
+
+int hto_merge(int out_bytes, uint64_t n, int c, const uint64_t* frontier, uint64_t nf, const uint64_t* partials,
+              uint64_t np, const uint64_t* S, uint64_t cap, uint64_t* out) {
+    hto_variant v; hto_layout lay;
+    int rc = check(out_bytes, n, cap, &v, &lay);
+    if (rc) return rc;
+    for (int r = 0; r < v.k; r++) {
+        uint64_t acc = 0;
+        for (uint64_t q = 0; q < np; q++) acc += partials[q * v.k + r];
+        out[r] = acc;
+    }
+    uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * 40 * (nf + 8));
+    uint64_t* nxt = (uint64_t*)malloc(sizeof(uint64_t) * 40 * (nf / 8 + 8));
+    memcpy(cur, frontier, sizeof(uint64_t) * 8 * v.k * nf);
+    int lvl = c;
+    while (nf >= 8) {
+        uint64_t nn = nf / 8, keep = nn & ~7ull;
+        for (uint64_t g = 0; g < nn; g++)
+            for (int r = 0; r < v.k; r++) {
+                uint64_t blk[8];
+                for (int j = 0; j < 8; j++) {
+                    uint64_t a = cur[(8 * g + 7) * 8 * v.k + r * 8 + j];
+                    for (int q = 0; q < 7; q++) a += nh(cur[(8 * g + q) * 8 * v.k + r * 8 + j], S[lay.T[r] + 7ull * lvl + q]);
+                    blk[j] = a;
+                }
+                if (g >= keep) out[r] += fin_term(&v, &lay, S, r, lvl + 1, g & 7, blk);
+                else memcpy(nxt + g * 8 * v.k + r * 8, blk, 64);
+            }
+        uint64_t* t = cur; cur = nxt; nxt = t;
+        nf = keep;
+        lvl++;
+    }
+    free(cur); free(nxt);
+    return 0;
+}

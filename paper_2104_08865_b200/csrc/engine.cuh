@@ -208,6 +208,15 @@ struct Params {
   u64* acc;       // per multi-job string: k partial digest words (self-resetting)
   u32* events;    // per multi-job string: completion events seen (self-resetting)
   int job_lvl;    // a warp job is one level-`job_lvl` subtree
+  // slice mode (one string split across GPUs, fixed mode with n_strings = 1):
+  // jobs cover global instances [slice_inst0, ...); finished non-leftover
+  // blocks at frontier_lvl go to `frontier` (index - frontier_base) instead
+  // of merging further, and every finalize term accumulates into acc[0..k)
+  // (no digest is written; hth_hash_merge completes it).
+  int frontier_lvl;  // 0 = off
+  u64 slice_job0;    // global jq of the slice's first job
+  u64 frontier_base;
+  u64* frontier;
   // EHC seed words S[0..e*w), split into halves.  The kernel takes Params as
   // a __grid_constant__, so these are constant-bank operands of the NH adds.
   // Interleaved (lo, hi) so one 64-bit constant load fetches both halves.
@@ -247,6 +256,9 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u3
     st.cnt = s * P.cnt_per;
   }
   st.s = s;
+  if (!VARLEN && P.frontier_lvl) {  // slice mode: P.n_bytes is the whole string
+    jq += (u32)P.slice_job0;
+  }
   st.n_inst = ((st.n + 7) >> 3) / M;
   st.L = st.n_inst ? level_count(st.n_inst) : 1;
   st.J = (u32)job_count(st.n_inst, P.job_lvl);

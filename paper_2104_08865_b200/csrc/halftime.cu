@@ -12,6 +12,7 @@
 #include "../../include/halftime_b200.h"
 #include "hash_kernel.cuh"
 #include "tail_kernel.cuh"
+#include "merge_kernel.cuh"
 
 using namespace hth;
 
@@ -564,6 +565,115 @@ int hth_varlen_status(void* d_workspace, void* stream) {
   CK(cudaMemcpyAsync(&h, d_workspace, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   if (h) return fail(HTH_ESEEDSIZE, "a string was longer than max_n_bytes; its digest is invalid");
+  return HTH_OK;
+}
+
+// ---- one string split across devices (config 5) ----------------------
+int hth_slice_plan(int output_bytes, uint64_t n_bytes, uint64_t n_slices, uint64_t* inst_bounds,
+                   int* frontier_level, uint64_t* frontier_counts) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (!n_slices || !inst_bounds || !frontier_level || !frontier_counts) return fail(HTH_EINVAL, "bad slice plan args");
+  const u64 n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
+  const int jl = pick_job_lvl(n_inst);
+  // frontier level: the largest c >= job level leaving >= 64 level-c subtrees
+  // per slice (load balance within one subtree per 64)
+  int c = jl;
+  while ((n_inst >> (3 * (c + 1))) >= 64 * n_slices) c++;
+  const u64 sub = 1ull << (3 * c), nsub = n_inst / sub;
+  for (u64 i = 0; i <= n_slices; i++) inst_bounds[i] = (nsub * i / n_slices) * sub;
+  inst_bounds[n_slices] = n_inst;  // the last slice also takes the ragged end and the tail
+  const u64 keep = (n_inst >> (3 * c)) & ~7ull;  // non-leftover level-c blocks
+  for (u64 i = 0; i < n_slices; i++) {
+    const u64 a = inst_bounds[i] >> (3 * c), b = std::min(inst_bounds[i + 1] >> (3 * c), keep);
+    frontier_counts[i] = b > a ? b - a : 0;
+  }
+  *frontier_level = c;
+  return HTH_OK;
+}
+
+int hth_workspace_size_slice(int output_bytes, uint64_t n_bytes, uint64_t* bytes) {
+  return hth_workspace_size_fixed(output_bytes, 1, n_bytes, bytes);
+}
+
+int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
+                   int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
+                   uint64_t* d_frontier, uint64_t* d_partial, void* d_workspace, uint64_t workspace_bytes,
+                   void* stream) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
+  const FixedPlan f = fixed_plan(v, 1, n_bytes);
+  const u64 per = 1ull << (3 * f.job_lvl), sub = 1ull << (3 * frontier_level);
+  if (frontier_level < f.job_lvl || inst_begin % sub || inst_begin > inst_end || inst_end > f.n_inst ||
+      (inst_end != f.n_inst && inst_end % sub))
+    return fail(HTH_EINVAL, "slice bounds must be multiples of 8^frontier_level instances (frontier >= %d)", f.job_lvl);
+  if (!d_partial || !d_seed) return fail(HTH_EINVAL, "null device pointer");
+  if (reinterpret_cast<uintptr_t>(d_slice) & 15) return fail(HTH_EINVAL, "d_slice must be 16-byte aligned");
+  if (workspace_bytes < f.ws_total) return fail(HTH_EINVAL, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(d_partial, 0, v.k * 8, st));
+  const bool last = inst_end == f.n_inst;
+  const u64 j0 = inst_begin / per;
+  const u64 j1 = last ? f.J : inst_end / per;
+  if (j1 <= j0) return HTH_OK;
+  const u64 byte0 = inst_begin * (u64)v.m * 8;
+  Params P{};
+  P.data = (const uint8_t*)d_slice - byte0;  // global byte b of the string lives at d_slice[b - byte0]
+  P.n_strings = 1;
+  P.stride = 0;
+  P.n_bytes = n_bytes;
+  P.J_fixed = f.J;
+  P.n_jobs = j1 - j0;
+  P.S = d_seed;
+  P.out = d_partial;
+  P.job_lvl = f.job_lvl;
+  P.frontier_lvl = frontier_level;
+  P.slice_job0 = j0;
+  P.frontier_base = inst_begin >> (3 * frontier_level);
+  P.frontier = d_frontier;
+  fill_ehc(v, seed_fold, P);
+  uint8_t* ws = (uint8_t*)d_workspace;
+  P.scratch = (u64*)ws;
+  P.acc = d_partial;
+  P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
+  P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
+  return dispatch<false>(output_bytes, P, P.n_jobs, st);
+}
+
+int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
+                   uint64_t n_frontier, const uint64_t* d_partials, uint64_t n_partials, uint64_t seed_fold,
+                   const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out, void* d_workspace,
+                   uint64_t workspace_bytes, void* stream) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
+  (void)seed_fold;
+  const u64 n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
+  const u64 keep = (n_inst >> (3 * frontier_level)) & ~7ull;
+  if (n_frontier != keep)
+    return fail(HTH_EINVAL, "frontier holds %llu blocks, expected %llu", (unsigned long long)n_frontier,
+                (unsigned long long)keep);
+  const u64 need = 2 * (n_frontier / 8 + 8) * 8ull * v.k * 8;
+  if (workspace_bytes < need) return fail(HTH_EINVAL, "merge workspace too small: need %llu", (unsigned long long)need);
+  MergeParams M{};
+  M.n_bytes = n_bytes;
+  M.c = frontier_level;
+  M.frontier = d_frontier;
+  M.nf = n_frontier;
+  M.partials = d_partials;
+  M.np = n_partials;
+  M.S = d_seed;
+  M.tmp = (u64*)d_workspace;
+  M.out = d_out;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (output_bytes) {
+    case 16: merge_kernel<16><<<1, 256, 0, st>>>(M); break;
+    case 24: merge_kernel<24><<<1, 256, 0, st>>>(M); break;
+    case 32: merge_kernel<32><<<1, 256, 0, st>>>(M); break;
+    case 40: merge_kernel<40><<<1, 256, 0, st>>>(M); break;
+  }
+  CK(cudaGetLastError());
   return HTH_OK;
 }
 

@@ -141,6 +141,14 @@ __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeC
       }
       return 1;
     }
+    if (P.frontier_lvl && lvl == P.frontier_lvl) {
+      // slice mode: hand the subtree root to hth_hash_merge
+      if (lane < 8) {
+#pragma unroll
+        for (int r = 0; r < K; r++) P.frontier[(idx - P.frontier_base) * 8 * K + r * 8 + j] = B[r];
+      }
+      return 0;
+    }
     u64 woff = 0, coff = 0;
     for (int l = P.job_lvl; l <= lvl; l++) {
       const u64 ln = st.n_inst >> (3 * l);
@@ -400,7 +408,10 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       const u64 v = warp_sum(fin[r]);
       if (lane == r) mine = v;
     }
-    if (st.J == 1) {
+    if (P.frontier_lvl) {
+      // slice mode: accumulate only; the merge step publishes the digest
+      if (lane < K && mine) atomicAdd(reinterpret_cast<unsigned long long*>(P.acc) + lane, (unsigned long long)mine);
+    } else if (st.J == 1) {
       if (lane < K) P.out[st.s * K + lane] = mine;
     } else if (events) {
       // multi-job string: add this job's finalize terms, then count its

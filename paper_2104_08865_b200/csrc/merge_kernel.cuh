@@ -1,0 +1,77 @@
+// HalftimeHash B200 engine: top-of-tree merge for one string hashed in
+// slices (config 5 across GPUs).  Each slice (hth_hash_slice) leaves its
+// finished, non-leftover level-c subtree roots ("frontier") and a partial
+// digest.  This kernel continues the reference's stack construction from
+// level c over the gathered frontier (tree.py:63-100, level seeds
+// tree.py:55-60), adds the finalize terms of the leftovers it produces
+// (tree.py:103-134) and the slices' partials, and writes the digest.
+#pragma once
+#include "engine.cuh"
+
+namespace hth {
+
+struct MergeParams {
+  u64 n_bytes;
+  int c;                 // frontier level
+  const u64* frontier;   // nf blocks [idx][r][lane] at level c, global order
+  u64 nf;                // = (n_inst >> 3c) & ~7
+  const u64* partials;   // np x k partial digests
+  u64 np;
+  const u64* S;
+  u64* tmp;              // nf/8 * 8k words scratch (ping-pong half)
+  u64* out;              // k words
+};
+
+template <int OUT>
+__global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ MergeParams P) {
+  constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m, EW = Geo<Var<OUT>>::ew;
+  __shared__ unsigned long long red[K];
+  const u64 n_inst = ((P.n_bytes + 7) >> 3) / M;
+  const u64 L = n_inst ? level_count(n_inst) : 1;
+  u64 fin[K];
+#pragma unroll
+  for (int r = 0; r < K; r++) fin[r] = 0;
+  if (threadIdx.x < K) red[threadIdx.x] = 0;
+  const u64* cur = P.frontier;
+  u64* bufs[2] = {P.tmp, P.tmp + (P.nf / 8 + 8) * 8 * K};
+  u64 nf = P.nf;
+  int lvl = P.c, flip = 0;
+  __syncthreads();
+  while (nf >= 8) {
+    const u64 nn = nf / 8, keep = nn & ~7ull;  // nodes at lvl+1; complete-group ones carry on
+    u64* nxt = bufs[flip];
+    for (u64 it = threadIdx.x; it < nn * K * 8; it += blockDim.x) {
+      const u64 g = it / (K * 8);
+      const int r = (int)((it / 8) % K), j = (int)(it % 8);
+      const u64* blk = cur + g * 8 * 8 * K + r * 8 + j;
+      const u64* s = P.S + (u64)EW + 7ull * L * r + 7ull * lvl;
+      u64 v = blk[7 * 8 * K];
+#pragma unroll
+      for (int q = 0; q < 7; q++) v = nh_acc(v, blk[q * 8 * K], __ldg(s + q));
+      if (g >= keep) {  // leftover at level lvl+1 -> finalize slot
+        const u64 F = (u64)EW + 7ull * L * K + 64ull * L * r;
+#pragma unroll
+        for (int rr = 0; rr < K; rr++)
+          if (rr == r) fin[rr] = nh_acc(fin[rr], v, __ldg(P.S + F + 56ull * (lvl + 1) + (g & 7) * 8 + j));
+      } else {
+        nxt[g * 8 * K + r * 8 + j] = v;
+      }
+    }
+    __syncthreads();
+    cur = nxt;
+    flip ^= 1;
+    nf = keep;
+    lvl++;
+  }
+#pragma unroll
+  for (int r = 0; r < K; r++)
+    if (fin[r]) atomicAdd(&red[r], (unsigned long long)fin[r]);
+  __syncthreads();
+  if (threadIdx.x < K) {
+    u64 v = red[threadIdx.x];
+    for (u64 p = 0; p < P.np; p++) v += P.partials[p * K + threadIdx.x];
+    P.out[threadIdx.x] = v;
+  }
+}
+
+}  // namespace hth

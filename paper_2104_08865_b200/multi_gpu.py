@@ -1,0 +1,162 @@
+"""Multi-GPU paths (one process per GPU, torch.distributed for the plumbing).
+
+* Batches of independent strings (configs 1-4) shard by string with no
+  data-path collective: ``shard_round_robin`` / ``shard_blocks``.
+* One huge string (config 5) splits at multiples of 8^c instances.  The
+  reference's stack construction groups blocks front-aligned
+  (halftimehash/tree.py:63-100), so each slice reduces to independent level-c
+  subtree roots; finalize terms (tree.py:103-134) and the Toeplitz tail
+  (hasher.py:186-206) are sums, so each slice also yields a partial digest.
+  The only exchange is gathering the roots (<= a few hundred KB) and the
+  partials to rank 0, which finishes the tree with ``hth_hash_merge``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .hasher import SeedBuffer, _check_capacity
+from .params import HashParams
+
+
+@dataclass(frozen=True)
+class SlicePlan:
+    params: HashParams
+    n_bytes: int
+    level: int  # frontier level c
+    bounds: tuple  # n_slices + 1 instance bounds (multiples of 8^c but the last)
+    counts: tuple  # frontier roots emitted by each slice
+
+    @property
+    def n_slices(self) -> int:
+        return len(self.counts)
+
+    @property
+    def n_frontier(self) -> int:
+        return sum(self.counts)
+
+    def byte_range(self, i: int):
+        """Bytes [b0, b1) of the string that slice i reads."""
+        ib = self.params.instance_words * 8
+        b0 = self.bounds[i] * ib
+        b1 = self.n_bytes if i == self.n_slices - 1 else self.bounds[i + 1] * ib
+        return b0, b1
+
+
+def slice_plan(params: HashParams, n_bytes: int, n_slices: int) -> SlicePlan:
+    b = (ctypes.c_uint64 * (n_slices + 1))()
+    lvl = ctypes.c_int()
+    cnt = (ctypes.c_uint64 * n_slices)()
+    _lib.check(_lib.lib().hth_slice_plan(params.output_bytes, n_bytes, n_slices, b, ctypes.byref(lvl), cnt))
+    return SlicePlan(params, n_bytes, lvl.value, tuple(int(x) for x in b), tuple(int(x) for x in cnt))
+
+
+def shard_round_robin(n_strings: int, rank: int, world: int) -> np.ndarray:
+    """Config 4: string s goes to rank s % world."""
+    return np.arange(rank, n_strings, world)
+
+
+def shard_blocks(n_strings: int, rank: int, world: int) -> range:
+    """Config 3: contiguous index ranges."""
+    lo = n_strings * rank // world
+    hi = n_strings * (rank + 1) // world
+    return range(lo, hi)
+
+
+_WS = {}
+
+
+def _ws(dev, nbytes):
+    import torch
+
+    t = _WS.get(dev.index)
+    if t is None or t.numel() < nbytes:
+        t = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=dev)
+        _WS[dev.index] = t
+    return t
+
+
+def hash_slice(data, plan: SlicePlan, i: int, seed: SeedBuffer):
+    """Hash slice i on data's GPU.  ``data``: CUDA uint8 tensor holding bytes
+    plan.byte_range(i).  Returns (frontier (count, 8k) int64, partial (k,) int64)."""
+    import torch
+
+    p = plan.params
+    _check_capacity(seed, p, plan.n_bytes)
+    dev = data.device
+    k = p.output_words
+    fr = torch.empty((max(plan.counts[i], 1), 8 * k), dtype=torch.int64, device=dev)
+    part = torch.empty(k, dtype=torch.int64, device=dev)
+    wsz = ctypes.c_uint64()
+    _lib.check(_lib.lib().hth_workspace_size_slice(p.output_bytes, plan.n_bytes, ctypes.byref(wsz)))
+    ws = _ws(dev, wsz.value)
+    b0, b1 = plan.byte_range(i)
+    if data.numel() < b1 - b0:
+        raise ValueError("slice tensor shorter than its byte range")
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().hth_hash_slice(
+            p.output_bytes, data.data_ptr(), plan.n_bytes, plan.bounds[i], plan.bounds[i + 1], plan.level, seed.fold,
+            seed.device_words(dev).data_ptr(), seed.capacity, fr.data_ptr(), part.data_ptr(), ws.data_ptr(),
+            ws.numel(), st))
+    return fr[:plan.counts[i]], part
+
+
+def hash_merge(frontier, partials, plan: SlicePlan, seed: SeedBuffer):
+    """Finish the tree from the gathered frontier (n_frontier, 8k) and partials (n, k)."""
+    import torch
+
+    p = plan.params
+    dev = frontier.device if frontier.numel() else partials.device
+    k = p.output_words
+    out = torch.empty(k, dtype=torch.int64, device=dev)
+    need = 2 * (plan.n_frontier // 8 + 8) * 8 * k * 8
+    tmp = torch.empty(need, dtype=torch.uint8, device=dev)
+    fr = frontier.contiguous()
+    pa = partials.contiguous()
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(_lib.lib().hth_hash_merge(
+            p.output_bytes, plan.n_bytes, plan.level, fr.data_ptr() if fr.numel() else None, plan.n_frontier,
+            pa.data_ptr(), pa.shape[0], seed.fold, seed.device_words(dev).data_ptr(), seed.capacity,
+            out.data_ptr(), tmp.data_ptr(), tmp.numel(), st))
+    return out
+
+
+def hash_string_distributed(local, plan: SlicePlan, seed: SeedBuffer, group=None, slice_fn=None, merge_fn=None):
+    """Each rank hashes slice `rank` of one string; rank 0 returns the (k,)
+    digest words (numpy uint64), other ranks None.
+
+    The exchange is one all_gather of the padded frontier roots and one of the
+    partials (NCCL over NVLink on GPUs; gloo on CPU tensors in the tests).
+    ``slice_fn(local, plan, i, seed) -> (frontier, partial)`` and
+    ``merge_fn(frontier, partials, plan, seed) -> digest`` default to the CUDA
+    engine."""
+    import torch
+    import torch.distributed as dist
+
+    slice_fn = slice_fn or hash_slice
+    merge_fn = merge_fn or hash_merge
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    if world != plan.n_slices:
+        raise ValueError("plan must have one slice per rank")
+    k = plan.params.output_words
+    fr, part = slice_fn(local, plan, rank, seed)
+    maxc = max(max(plan.counts), 1)
+    pad = torch.zeros((maxc, 8 * k), dtype=torch.int64, device=part.device)
+    if fr.shape[0]:
+        pad[:fr.shape[0]] = fr
+    frs = [torch.empty_like(pad) for _ in range(world)]
+    parts = [torch.empty_like(part) for _ in range(world)]
+    dist.all_gather(frs, pad, group=group)
+    dist.all_gather(parts, part, group=group)
+    if rank != 0:
+        return None
+    frontier = torch.cat([frs[i][:plan.counts[i]] for i in range(world)], dim=0)
+    digest = merge_fn(frontier, torch.stack(parts), plan, seed)
+    return digest.cpu().numpy().view(np.uint64).copy()

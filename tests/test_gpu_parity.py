@@ -212,3 +212,63 @@ def test_hash_words_seam(hh):
     got = hh.hash_words(words, n_bytes, seed, p)
     want = o.hash_batch(o.variant(32), words, n_bytes, seed.words_np(0, seed.capacity))
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------ slices (config 5)
+@pytest.mark.parametrize("w", VARIANTS)
+def test_slices_and_merge_match_full(hh, w):
+    # emulate N ranks one after another on one GPU (no kernel waits on another)
+    import torch
+
+    from paper_2104_08865_b200 import multi_gpu
+
+    v = o.variant(w)
+    for inst in (600, 8 ** 4 + 8 ** 3 * 3 + 11, 8 ** 5 * 2 + 8 ** 4 + 5):
+        n = inst * v.m * 8 + 45
+        buf = hh.fill_bytes(n, 12)
+        p = hh.variant(w)
+        seed = hh.seed_for_input(bytes(range(32)), p, n)
+        full = _u64(hh.hash_fixed(buf, n, seed, p))[0]
+        host = np.frombuffer(o.fill_bytes(n, 12), dtype=np.uint8).copy()
+        want = coracle.hash_one(w, host, seed.words_np(0, seed.capacity))
+        assert np.array_equal(full, want)
+        for ns in (1, 2, 3, 8):
+            plan = multi_gpu.slice_plan(p, n, ns)
+            frs, parts = [], []
+            for i in range(ns):
+                b0, b1 = plan.byte_range(i)
+                fr, part = multi_gpu.hash_slice(buf[b0:], plan, i, seed)
+                frs.append(fr.clone())
+                parts.append(part.clone())
+            got = multi_gpu.hash_merge(torch.cat(frs), torch.stack(parts), plan, seed)
+            assert np.array_equal(_u64(got), want), (w, inst, ns)
+
+
+@pytest.mark.slow
+def test_config5_full_16gib(hh):
+    # config 5: one 16 GiB string, 16-byte variant; GPU single-device digest,
+    # 8-slice decomposition and the threaded C oracle must all agree
+    import torch
+
+    from paper_2104_08865_b200 import multi_gpu
+    from workloads import DATA_SEED, MASTER
+
+    n = 16 << 30
+    p = hh.variant(16)
+    buf = hh.fill_bytes(n, DATA_SEED)
+    seed = hh.seed_for_input(MASTER, p, n)
+    full = _u64(hh.hash_fixed(buf, n, seed, p))[0]
+    plan = multi_gpu.slice_plan(p, n, 8)
+    frs, parts = [], []
+    for i in range(8):
+        b0, _ = plan.byte_range(i)
+        fr, part = multi_gpu.hash_slice(buf[b0:], plan, i, seed)
+        frs.append(fr.clone())
+        parts.append(part.clone())
+    sliced = _u64(multi_gpu.hash_merge(torch.cat(frs), torch.stack(parts), plan, seed))
+    del buf
+    torch.cuda.empty_cache()
+    host = coracle.splitmix(DATA_SEED, 0, n // 8).view(np.uint8)
+    want = coracle.hash_huge(16, host, seed.words_np(0, seed.capacity))
+    assert np.array_equal(full, want)
+    assert np.array_equal(sliced, want)
