@@ -433,7 +433,7 @@ def arm_ours(args, rank, world, local_rank):
                        "parallelism": f"dp{world} (independent strings, no collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(workload),
-                         "kernel": "hash_kernel<40,false,4,4>", "kernel_ms": kernel_ms,
+                         "kernel": "hash_kernel<40,false,W=2,NS=2,MINB=4>", "kernel_ms": kernel_ms,
                          "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
