@@ -13,7 +13,7 @@ import threading
 from ._errors import SeedSizeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhalftime_b200.so")
+LIB_PATH = os.environ.get("HTH_LIB") or os.path.join(_HERE, "libhalftime_b200.so")
 
 HTH_OK, HTH_EINVAL, HTH_ESEEDSIZE, HTH_ERANGE, HTH_ECUDA, HTH_ENOMEM = 0, -1, -2, -3, -4, -5
 

@@ -149,15 +149,27 @@ template <int OUT> struct KCfg;
 // W warps per CTA, NS ring stages per warp (one 8-instance round each),
 // MINB CTAs per SM the register allocation must allow.
 template <> struct KCfg<16> { static constexpr int W = 4, NS = 2, MINB = 4; };
-template <> struct KCfg<24> { static constexpr int W = 2, NS = 2, MINB = 4; };
-template <> struct KCfg<32> { static constexpr int W = 2, NS = 2, MINB = 4; };
-template <> struct KCfg<40> { static constexpr int W = 2, NS = 2, MINB = 4; };
+#ifndef HTH_V2432_MINB
+#define HTH_V2432_MINB 4
+#endif
+template <> struct KCfg<24> { static constexpr int W = 2, NS = 2, MINB = HTH_V2432_MINB; };
+template <> struct KCfg<32> { static constexpr int W = 2, NS = 2, MINB = HTH_V2432_MINB; };
+#ifndef HTH_V40_W
+#define HTH_V40_W 2
+#endif
+#ifndef HTH_V40_NS
+#define HTH_V40_NS 2
+#endif
+#ifndef HTH_V40_MINB
+#define HTH_V40_MINB 6
+#endif
+template <> struct KCfg<40> { static constexpr int W = HTH_V40_W, NS = HTH_V40_NS, MINB = HTH_V40_MINB; };
 
 template <int OUT>
 constexpr size_t smem_bytes() {
   constexpr int M = Geo<Var<OUT>>::m;
   constexpr size_t SB = ROUND_INST * M * 8 + 128;
-  return KCfg<OUT>::W * KCfg<OUT>::NS * (SB + 8);
+  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 2 * Var<OUT>::k * 8 * 8);
 }
 
 int sm_count(int dev) {

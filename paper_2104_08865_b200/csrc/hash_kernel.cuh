@@ -3,6 +3,10 @@
 #pragma once
 #include "engine.cuh"
 
+#ifndef HTH_S1_REGS
+#define HTH_S1_REGS 1
+#endif
+
 namespace hth {
 
 // Little-endian u64 word `widx` of a stage whose first string byte sits at
@@ -198,6 +202,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   const int q = lane >> 3, j = lane & 7;
   uint8_t* ring = smem + warp * NS * SB;
   u64* bars = reinterpret_cast<u64*>(smem + W * NS * SB) + warp * NS;
+  // level-2 / level-3 node accumulators of this warp, [level][r][lane 0..7];
+  // touched once per round at most, so they live in shared memory, not registers
+  u64* nacc = reinterpret_cast<u64*>(smem + W * NS * SB + W * NS * 8) + warp * 2 * K * 8;
   if (lane == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -251,10 +258,11 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
 
   // ---- consumer ----
   u32 cseq = 0;
-  u32 seedL = 0;                 // layout level count the cached tree seeds belong to
-  u64 s1A[K], s1B[K];            // level-1 node seeds of this thread's two positions
   TreeCtx<K, Geo<V>::ew> tc;
-  tc.L = 0;
+#if HTH_S1_REGS
+  u32 seedL = 0;
+  u64 s1A[K], s1B[K];  // level-1 node seeds of this thread's two positions
+#endif
   for (u64 job = gw; job < n_jobs; job += NW) {
     Str st;
     u32 jq, ninst;
@@ -264,9 +272,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     const u32 nchunks = (u32)ceil_div(nbytes, CB);
     const u32 delta = (u32)(reinterpret_cast<uintptr_t>(st.p) & 15);
     const bool last_job = (jq + 1 == st.J);
+    tc.L = st.L;  // tree seeds depend on the layout (hasher.py:130-153) via L only
+#if HTH_S1_REGS
     if (st.L != seedL) {
-      // tree seeds depend on the layout (hasher.py:130-153) via L only
-      tc.L = st.L;
 #pragma unroll
       for (int r = 0; r < K; r++) {
         s1A[r] = __ldg(S + tc.T(r) + q);
@@ -274,11 +282,16 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       }
       seedL = st.L;
     }
+#endif
 
-    u64 fin[K], n2[K], n3[K];
+    u64 fin[K];
     u32 events = last_job ? 1u : 0u;
 #pragma unroll
-    for (int r = 0; r < K; r++) fin[r] = n2[r] = n3[r] = 0;
+    for (int r = 0; r < K; r++) fin[r] = 0;
+    if (lane < 8) {
+#pragma unroll
+      for (int r = 0; r < 2 * K; r++) nacc[r * 8 + lane] = 0;
+    }
     const u64 inst0 = (u64)jq << (3 * job_lvl);
     const u64 full0 = st.n_inst & ~7ull;  // instances in complete level-1 groups
     const u64 len1 = st.n_inst >> 3, full1 = len1 & ~7ull;
@@ -310,8 +323,14 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
           u64 B1[K];
 #pragma unroll
           for (int r = 0; r < K; r++) {
+            // level-0 seeds S[T_r + q] (tree.py:55-60); L1-resident
+#if HTH_S1_REGS
             u64 v = nh_acc(0, CA[r], s1A[r]);
             v = (q < 3) ? nh_acc(v, CB_[r], s1B[r]) : v + CB_[r];
+#else
+            u64 v = nh_acc(0, CA[r], __ldg(S + tc.T(r) + q));
+            v = (q < 3) ? nh_acc(v, CB_[r], __ldg(S + tc.T(r) + q + 4)) : v + CB_[r];
+#endif
             v += shfl_xor(v, 8);
             v += shfl_xor(v, 16);
             B1[r] = v;
@@ -325,33 +344,47 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
           } else {
             if (q == 0) {
 #pragma unroll
-              for (int r = 0; r < K; r++)
-                n2[r] = (p1 < 7) ? nh_acc(n2[r], B1[r], __ldg(S + tc.T(r) + 7 + p1)) : n2[r] + B1[r];
+              for (int r = 0; r < K; r++) {
+                const u64 a = nacc[r * 8 + j];
+                nacc[r * 8 + j] = (p1 < 7) ? nh_acc(a, B1[r], __ldg(S + tc.T(r) + 7 + p1)) : a + B1[r];
+              }
             }
+            __syncwarp();
             if (p1 == 7) {
-              const u64 G2 = G1 >> 3;  // level-2 block complete in lanes 0-7
+              const u64 G2 = G1 >> 3;  // level-2 block complete (lanes 0-7)
+              u64 B2[K];
+#pragma unroll
+              for (int r = 0; r < K; r++) {
+                B2[r] = lane < 8 ? nacc[r * 8 + j] : 0;
+                if (lane < 8) nacc[r * 8 + j] = 0;
+              }
               if (job_lvl == 2) {
-                events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, n2, fin, lane);
+                events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, B2, fin, lane);
               } else {
                 const int p2 = (int)(G2 & 7);
                 if (lane < 8) {
                   if (G2 >= full2) {
 #pragma unroll
-                    for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], n2[r], __ldg(S + tc.F(r) + 112 + p2 * 8 + j));
+                    for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B2[r], __ldg(S + tc.F(r) + 112 + p2 * 8 + j));
                   } else {
 #pragma unroll
-                    for (int r = 0; r < K; r++)
-                      n3[r] = (p2 < 7) ? nh_acc(n3[r], n2[r], __ldg(S + tc.T(r) + 14 + p2)) : n3[r] + n2[r];
+                    for (int r = 0; r < K; r++) {
+                      const u64 a = nacc[(K + r) * 8 + j];
+                      nacc[(K + r) * 8 + j] = (p2 < 7) ? nh_acc(a, B2[r], __ldg(S + tc.T(r) + 14 + p2)) : a + B2[r];
+                    }
                   }
                 }
+                __syncwarp();
                 if (G2 < full2 && p2 == 7) {
-                  events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, n3, fin, lane);
+                  u64 B3[K];
 #pragma unroll
-                  for (int r = 0; r < K; r++) n3[r] = 0;
+                  for (int r = 0; r < K; r++) {
+                    B3[r] = lane < 8 ? nacc[(K + r) * 8 + j] : 0;
+                    if (lane < 8) nacc[(K + r) * 8 + j] = 0;
+                  }
+                  events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, B3, fin, lane);
                 }
               }
-#pragma unroll
-              for (int r = 0; r < K; r++) n2[r] = 0;
             }
           }
         } else {
