@@ -289,29 +289,43 @@ def measure_workload(hh, torch, workload, steps, warmup, peak):
     return res
 
 
-def e2e_fixed(hh, torch, workload, steps, n_strings_cap=None):
-    """Public host-buffer API (hth_hash_fixed_host) from pinned memory: H2D + hash + D2H per step."""
+def e2e_fixed(hh, torch, workload, steps, n_strings_cap=None, rank=0, world=1, local_rank=0, dist=None):
+    """Public host-buffer API (hth_hash_fixed_host) from pinned memory on every
+    rank at once: H2D + hash + D2H per step; value = all ranks' bytes / the
+    slowest rank's wall time (barrier on both sides of each step)."""
     cfg = wl.CONFIGS[workload]
     w, n, B = cfg["variant"], cfg["n_bytes"], cfg["n_strings"]
     if n_strings_cap:
         B = min(B, n_strings_cap)
     p = hh.variant(w)
-    dev = torch.empty(B * n + 16, dtype=torch.uint8, device="cuda")
-    hh.fill_bytes(B * n, wl.DATA_SEED, 0, out=dev)
+    ctx = setup_fixed(hh, torch, workload, rank, world) if not n_strings_cap else None
+    if ctx is None:
+        dev = torch.empty(B * n + 16, dtype=torch.uint8, device="cuda")
+        hh.fill_bytes(B * n, wl.DATA_SEED, rank * B * n // 8, out=dev)
+    else:
+        dev = ctx["buf"]
     host = torch.empty(B * n, dtype=torch.uint8, pin_memory=True)
     host.copy_(dev[:B * n])
-    del dev
+    del dev, ctx
     torch.cuda.empty_cache()
-    hh.hash_fixed_host(host, B, n, wl.MASTER, p)  # warm-up (allocates staging buffers)
+    hh.hash_fixed_host(host, B, n, wl.MASTER, p, device=local_rank)  # warm-up (allocates staging buffers)
     times = []
     for _ in range(steps):
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
-        out = hh.hash_fixed_host(host, B, n, wl.MASTER, p)
-        times.append(time.perf_counter() - t0)
+        out = hh.hash_fixed_host(host, B, n, wl.MASTER, p, device=local_rank)
+        dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        times.append(dt)
     dt = statistics.median(times)
-    return {"value": B * n / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": B * n,
-            "d2h_bytes_per_step": B * p.output_words * 8, "strings_per_step": B,
-            "steps": steps, "api": "hth_hash_fixed_host (pinned host memory, 3-stream chunked H2D/hash/D2H)"}, out
+    return {"value": world * B * n / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": world * B * n,
+            "d2h_bytes_per_step": world * B * p.output_words * 8, "strings_per_step": world * B,
+            "steps": steps, "api": "hth_hash_fixed_host (pinned host memory, 3-stream chunked H2D/hash/D2H), "
+                                   "all ranks concurrently, max-over-ranks wall time"}, out
 
 
 # ---------------------------------------------------------------- arms
@@ -399,10 +413,9 @@ def arm_ours(args, rank, world, local_rank):
     del ctx
     torch.cuda.empty_cache()
     e2e = None
-    if rank == 0 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:
         try:
-            e2e, _ = e2e_fixed(hh, torch, workload, args.e2e_steps, args.e2e_strings)
-            e2e["value"] *= 1.0
+            e2e, _ = e2e_fixed(hh, torch, workload, args.e2e_steps, args.e2e_strings, rank, world, local_rank, dist)
         except Exception as ex:  # pragma: no cover - report, do not hide
             e2e = {"value": None, "unit": UNIT, "error": repr(ex), "h2d_bytes_per_step": None,
                    "d2h_bytes_per_step": None}

@@ -207,6 +207,8 @@ struct Params {
   u32* counters;  // per-group arrival counts (self-resetting)
   u64* acc;       // per multi-job string: k partial digest words (self-resetting)
   u32* events;    // per multi-job string: completion events seen (self-resetting)
+  unsigned long long* job_ctr;  // dynamic job claiming (self-resetting)
+  u32* exit_ctr;                 // warps finished (self-resetting)
   int job_lvl;    // a warp job is one level-`job_lvl` subtree
   // slice mode (one string split across GPUs, fixed mode with n_strings = 1):
   // jobs cover global instances [slice_inst0, ...); finished non-leftover

@@ -79,6 +79,12 @@ void fill_ehc(const VarInfo& v, u64 fold, Params& P) {
   }
 }
 
+// dynamic job-claim counter and exit counter (zero-filled, self-resetting)
+void set_ctl(Params& P, uint8_t* ctl) {
+  P.job_ctr = reinterpret_cast<unsigned long long*>(ctl);
+  P.exit_ctr = reinterpret_cast<u32*>(ctl + 8);
+}
+
 u64 fold_of(const uint8_t* m) {
   u64 w[4];
   memcpy(w, m, 32);
@@ -169,7 +175,8 @@ template <int OUT>
 constexpr size_t smem_bytes() {
   constexpr int M = Geo<Var<OUT>>::m;
   constexpr size_t SB = ROUND_INST * M * 8 + 128;
-  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 2 * Var<OUT>::k * 8 * 8);
+  // ring + mbarriers + level-2/3 accumulators + claimed-job queue, per warp
+  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 2 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8);
 }
 
 int sm_count(int dev) {
@@ -281,13 +288,13 @@ FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
   f.ws_acc = multi ? align_up(n_strings * v.k * 8, 256) : 0;
   f.ws_cnt = align_up(n_strings * f.cnt_per * 4, 256);
   f.ws_ev = multi ? align_up(n_strings * 4, 256) : 0;
-  f.ws_total = f.ws_scratch + f.ws_acc + f.ws_cnt + f.ws_ev;
+  f.ws_total = f.ws_scratch + f.ws_acc + f.ws_cnt + f.ws_ev + 256;  // + job/exit counters
   return f;
 }
 
 // varlen workspace geometry
 struct VarPlan {
-  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_acc, off_ev, off_cub, cub_bytes, total, max_jobs,
+  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_acc, off_ev, off_ctl, off_cub, cub_bytes, total, max_jobs,
       scr_words, cnts;
 };
 int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
@@ -310,6 +317,7 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
   p->off_cnt = o; o = align_up(o + p->cnts * 4, 256);
   p->off_acc = o; o = align_up(o + n * v.k * 8, 256);
   p->off_ev = o; o = align_up(o + n * 4, 256);
+  p->off_ctl = o; o += 256;
   p->off_cub = o; o = align_up(o + cub_bytes, 256);
   p->total = o;
   return HTH_OK;
@@ -501,6 +509,7 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.acc = (u64*)(ws + f.ws_scratch);
   P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
   P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
+  set_ctl(P, ws + f.ws_total - 256);
   return dispatch<false>(output_bytes, P, f.n_jobs, st);
 }
 
@@ -568,6 +577,7 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   P.counters = (u32*)(ws + p.off_cnt);
   P.acc = (u64*)(ws + p.off_acc);
   P.events = (u32*)(ws + p.off_ev);
+  set_ctl(P, ws + p.off_ctl);
   return dispatch<true>(output_bytes, P, p.max_jobs, st);
 }
 
@@ -650,6 +660,7 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   P.acc = d_partial;
   P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
   P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
+  set_ctl(P, ws + f.ws_total - 256);
   return dispatch<false>(output_bytes, P, P.n_jobs, st);
 }
 

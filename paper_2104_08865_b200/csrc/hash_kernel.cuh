@@ -3,6 +3,9 @@
 #pragma once
 #include "engine.cuh"
 
+#ifndef HTH_STATIC_FIRST
+#define HTH_STATIC_FIRST 1
+#endif
 #ifndef HTH_S1_REGS
 #define HTH_S1_REGS 1
 #endif
@@ -212,58 +215,86 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   }
   __syncwarp();
 
-  const u64 NW = (u64)gridDim.x * W;
-  const u64 gw = (u64)blockIdx.x * W + warp;
   const u64 n_jobs = VARLEN ? P.meta[3 * P.n_strings] : P.n_jobs;
   const int job_lvl = P.job_lvl;
   const u64* __restrict__ S = P.S;
   const u64 pol = policy_evict_first();
 
-  // ---- producer cursor (uniform across the warp; lane 0 issues) ----
-  u64 pjob = gw;
-  u32 pchunk = 0, pnchunks = 0, pseq = 0;
+  // ---- producer: claims jobs dynamically (one atomic per job, lane 0) and
+  // keeps the ring NS chunks ahead of the consumer; claimed job ids are
+  // queued in shared memory so the consumer sees the same sequence.
+  // Jobs are claimed in index order: fixed mode is jq-major (full jobs first),
+  // so dynamic claiming also bounds the tail by one job.
+  constexpr u32 QN = NS + 4;
+  u64* jq_buf = reinterpret_cast<u64*>(nacc + 2 * K * 8 * W - warp * 2 * K * 8) + warp * QN;
+  u32 qhead = 0, qtail = 0;        // queue: [qtail, qhead) claimed, not yet started
+  bool pdone = false;
+  // the first job of every warp is static (job = global warp index), so the
+  // first bulk copy needs no atomic round trip; later claims start past it
+  const u64 n_warps = (u64)gridDim.x * W;
+  // small batches (one job per warp at most) never touch the counters
+  const bool claims = n_jobs > n_warps;
+  bool first = HTH_STATIC_FIRST || !claims;
+  u32 pchunk = 0, pnchunks = 0, pseq = 0, cseq = 0;
   const uint8_t* pbase = nullptr;
   u64 pbytes = 0;
-  auto p_load = [&]() {
-    Str st;
-    u32 jq, ni;
-    u64 b0;
-    decode_job<VARLEN, K, M>(P, pjob, st, jq);
-    job_span<M>(st, jq, job_lvl, b0, pbytes, ni);
-    pbase = st.p + b0;
-    pnchunks = (u32)ceil_div(pbytes, CB);
-    pchunk = 0;
-  };
   auto p_issue = [&]() {
-    while (pjob < n_jobs && pchunk >= pnchunks) {
-      pjob += NW;
-      if (pjob < n_jobs) p_load();
+    while (pseq - cseq < (u32)NS) {
+      if (pchunk >= pnchunks) {  // current producer job fully issued: claim the next
+        if (pdone || qhead - qtail >= QN) return;
+        unsigned long long jc = (u64)blockIdx.x * W + warp;
+        if (!first) {
+          if (!claims) {
+            pdone = true;
+            return;
+          }
+          if (lane == 0) jc = (HTH_STATIC_FIRST ? n_warps : 0) + atomicAdd(P.job_ctr, 1ull);
+          jc = __shfl_sync(0xffffffffu, jc, 0);
+        }
+        first = false;
+        if (jc >= n_jobs) {
+          pdone = true;
+          return;
+        }
+        if (lane == 0) jq_buf[qhead % QN] = jc;
+        qhead++;
+        Str st;
+        u32 jq, ni;
+        u64 b0;
+        decode_job<VARLEN, K, M>(P, jc, st, jq);
+        job_span<M>(st, jq, job_lvl, b0, pbytes, ni);
+        pbase = st.p + b0;
+        pnchunks = (u32)ceil_div(pbytes, CB);
+        pchunk = 0;
+        continue;
+      }
+      const u32 slot = pseq % NS;
+      const uint8_t* src = pbase + (u64)pchunk * CB;
+      const u64 len = min((u64)CB, pbytes - (u64)pchunk * CB);
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src) + len + 15) & ~uintptr_t(15);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bars[slot], (u32)(a1 - a0));
+        bulk_g2s(ring + slot * SB, reinterpret_cast<const void*>(a0), (u32)(a1 - a0), &bars[slot], pol);
+      }
+      pseq++;
+      pchunk++;
     }
-    if (pjob >= n_jobs) return;
-    const u32 slot = pseq % NS;
-    const uint8_t* src = pbase + (u64)pchunk * CB;
-    const u64 len = min((u64)CB, pbytes - (u64)pchunk * CB);
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
-    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src) + len + 15) & ~uintptr_t(15);
-    if (lane == 0) {
-      mbar_arrive_expect_tx(&bars[slot], (u32)(a1 - a0));
-      bulk_g2s(ring + slot * SB, reinterpret_cast<const void*>(a0), (u32)(a1 - a0), &bars[slot], pol);
-    }
-    pseq++;
-    pchunk++;
   };
-  if (pjob < n_jobs) p_load();
-#pragma unroll
-  for (int s = 0; s < NS; s++) p_issue();
+  p_issue();
 
   // ---- consumer ----
-  u32 cseq = 0;
   TreeCtx<K, Geo<V>::ew> tc;
 #if HTH_S1_REGS
   u32 seedL = 0;
   u64 s1A[K], s1B[K];  // level-1 node seeds of this thread's two positions
 #endif
-  for (u64 job = gw; job < n_jobs; job += NW) {
+  for (;;) {
+    if (qtail == qhead) p_issue();
+    if (qtail == qhead) break;  // no job left anywhere
+    __syncwarp();
+    const u64 job = jq_buf[qtail % QN];
+    qtail++;
     Str st;
     u32 jq, ninst;
     u64 byte0, nbytes;
@@ -460,6 +491,15 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
         if (lane < K) P.out[st.s * K + lane] = atomicExch(a + lane, 0ull);
         if (lane == 0) P.events[st.s] = 0;
       }
+    }
+  }
+  // every warp has stopped claiming; the last one out re-zeroes the counters
+  // (relaxed is enough: each warp's last claim returned before it got here)
+  if (claims && lane == 0) {
+    const u32 old = atomicAdd(P.exit_ctr, 1u);
+    if (old + 1 == gridDim.x * (u32)W) {
+      *P.job_ctr = 0;
+      *P.exit_ctr = 0;
     }
   }
 }
