@@ -188,10 +188,10 @@ int sm_count(int dev) {
   return cache[dev];
 }
 
-template <int OUT, bool VARLEN>
+template <int OUT, bool VARLEN, bool AL8>
 int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   constexpr int W = KCfg<OUT>::W, NS = KCfg<OUT>::NS;
-  auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB>;
+  auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB, AL8>;
   const size_t smem = smem_bytes<OUT>();
   static std::once_flag once[64];
   int dev = 0;
@@ -247,15 +247,22 @@ int dispatch_tail(const TailParams& P, u64 nch, cudaStream_t st) {
   return masked ? dispatch_tail_m<OUT, true>(P, nch, st) : dispatch_tail_m<OUT, false>(P, nch, st);
 }
 
-template <bool VARLEN>
-int dispatch(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
+template <bool VARLEN, bool AL8>
+int dispatch_al(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   switch (out) {
-    case 16: return launch_hash<16, VARLEN>(P, n_jobs_bound, st);
-    case 24: return launch_hash<24, VARLEN>(P, n_jobs_bound, st);
-    case 32: return launch_hash<32, VARLEN>(P, n_jobs_bound, st);
-    case 40: return launch_hash<40, VARLEN>(P, n_jobs_bound, st);
+    case 16: return launch_hash<16, VARLEN, AL8>(P, n_jobs_bound, st);
+    case 24: return launch_hash<24, VARLEN, AL8>(P, n_jobs_bound, st);
+    case 32: return launch_hash<32, VARLEN, AL8>(P, n_jobs_bound, st);
+    case 40: return launch_hash<40, VARLEN, AL8>(P, n_jobs_bound, st);
   }
   return fail(HTH_EINVAL, "unsupported output width %d", out);
+}
+// fixed batches whose strings all start 8-byte aligned get the aligned-only kernel
+template <bool VARLEN>
+int dispatch(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
+  if (!VARLEN && (reinterpret_cast<uintptr_t>(P.data) % 8) == 0 && P.stride % 8 == 0)
+    return dispatch_al<false, true>(out, P, n_jobs_bound, st);
+  return dispatch_al<VARLEN, false>(out, P, n_jobs_bound, st);
 }
 
 int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
