@@ -97,6 +97,16 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
                    uint64_t n_bytes, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
                    uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes, void* stream);
 
+/* ---- many seeds: the batched seam with per-row seed streams
+ * (hasher.py:331-413 with a (B, 1) fold array, tests/test_hasher.py:254-310).
+ * String s is hashed under the SeedBuffer whose fold is d_folds[s] (every
+ * seed word recomputed on the device, so there is no capacity to check).
+ * stride_bytes may be 0: one input hashed under n_strings seeds.  Workspace:
+ * hth_workspace_size_fixed, zero-filled once. */
+int hth_hash_fixed_folds(int output_bytes, const void* d_data, uint64_t n_strings, uint64_t stride_bytes,
+                         uint64_t n_bytes, const uint64_t* d_folds, uint64_t* d_out, void* d_workspace,
+                         uint64_t workspace_bytes, void* stream);
+
 /* ---- batched hash of variable-length strings packed in one buffer.
  * String s is d_data[d_offsets[s] .. d_offsets[s+1]) (u64 byte offsets on the
  * device, any alignment).  max_n_bytes: an upper bound on any string's

@@ -30,13 +30,15 @@ __all__ = [
     "Digest", "ErasureCode", "HashParams", "SeedBuffer", "SeedLayout", "SeedSizeError", "TransformMatrix",
     "VARIANTS", "digest", "expand_seed", "hash_bytes", "instance_count", "seed_for_input", "seed_layout",
     "seed_words_needed", "variant", "hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes",
+    "hash_fixed_folds", "hash_words_many_seeds",
     "__version__",
 ]
 
 
 def __getattr__(name):
     # batch entry points import torch lazily so host-only use stays light
-    if name in ("hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes"):
+    if name in ("hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes", "hash_fixed_folds",
+                "hash_words_many_seeds"):
         from . import batch
 
         return getattr(batch, name)

@@ -23,7 +23,7 @@ EXPORTS = (
     "hth_seed_layout", "hth_master_fold", "hth_expand_seed", "hth_fill_splitmix",
     "hth_workspace_size_fixed", "hth_hash_fixed", "hth_workspace_size_varlen",
     "hth_hash_varlen", "hth_varlen_status", "hth_hash_host", "hth_hash_fixed_host",
-    "hth_slice_plan", "hth_workspace_size_slice", "hth_hash_slice", "hth_hash_merge",
+    "hth_slice_plan", "hth_workspace_size_slice", "hth_hash_slice", "hth_hash_merge", "hth_hash_fixed_folds",
 )
 
 _lock = threading.Lock()
@@ -63,6 +63,7 @@ def lib() -> ctypes.CDLL:
             "hth_hash_host": [i32, vp, u64, ctypes.c_char_p, u64, vp, i32],
             "hth_hash_fixed_host": [i32, vp, u64, u64, u64, ctypes.c_char_p, u64, vp, i32],
             "hth_slice_plan": [i32, u64, u64, vp, pi32, vp],
+            "hth_hash_fixed_folds": [i32, vp, u64, u64, u64, vp, vp, vp, u64, vp],
             "hth_workspace_size_slice": [i32, u64, pu64],
             "hth_hash_slice": [i32, vp, u64, u64, u64, i32, u64, vp, u64, vp, vp, vp, u64, vp],
             "hth_hash_merge": [i32, u64, i32, vp, u64, vp, u64, u64, vp, u64, vp, vp, u64, vp],

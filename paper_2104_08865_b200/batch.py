@@ -20,7 +20,7 @@ from .hasher import SeedBuffer, _check_capacity, _check_params, seed_words_neede
 from .params import HashParams
 
 __all__ = ["hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes", "workspace_fixed",
-           "workspace_varlen"]
+           "workspace_varlen", "hash_fixed_folds", "hash_words_many_seeds"]
 
 
 def _stream(dev) -> int:
@@ -152,6 +152,47 @@ def hash_varlen(data: torch.Tensor, offsets, seed, params: HashParams, max_n_byt
             params.output_bytes, data.data_ptr(), d_off.data_ptr(), n, max_n_bytes, total, fold, seed_t.data_ptr(),
             cap, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(dev)))
     return out
+
+
+def hash_fixed_folds(data: torch.Tensor, n_bytes: int, folds, params: HashParams, n_strings: int = None,
+                     stride: int = None, out: torch.Tensor = None) -> torch.Tensor:
+    """Many seeds: string s hashed under the seed stream of folds[s]
+    (``_hash_words_np`` with a (B, 1) fold array, tests/test_hasher.py:254-310).
+    ``stride=0`` hashes one input under every fold.  Returns (B, k) int64."""
+    params = _check_params(params)
+    if not isinstance(data, torch.Tensor) or not data.is_cuda:
+        raise ValueError("data must be a CUDA tensor")
+    dev = data.device
+    f = folds if isinstance(folds, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(folds, dtype=np.uint64)).view(np.int64))
+    f = f.to(device=dev, dtype=torch.int64).contiguous()
+    n_strings = f.numel() if n_strings is None else n_strings
+    if f.numel() < n_strings:
+        raise ValueError("need one fold per string")
+    stride = n_bytes if stride is None else stride
+    if n_strings and (n_strings - 1) * stride + n_bytes > data.numel():
+        raise ValueError("data tensor too small")
+    k = params.output_words
+    if out is None:
+        out = torch.empty((n_strings, k), dtype=torch.int64, device=dev)
+    wsz = workspace_fixed(params, n_strings, n_bytes)
+    ws = _WS.get(dev, wsz)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().hth_hash_fixed_folds(
+            params.output_bytes, data.data_ptr(), n_strings, stride, n_bytes, f.data_ptr(), out.data_ptr(),
+            ws.data_ptr(), ws.numel(), _stream(dev)))
+    return out
+
+
+def hash_words_many_seeds(words, n_bytes: int, folds, params: HashParams, device=None) -> np.ndarray:
+    """One (n_words,) input -- or a (B, n_words) batch -- under B seed folds.
+    Returns (B, k) uint64 like the reference seam with a (B, 1) fold region."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    folds = np.asarray(folds, dtype=np.uint64).reshape(-1)
+    t = torch.from_numpy(w.view(np.uint8).reshape(-1)).cuda(device)
+    stride = 0 if w.ndim == 1 else w.shape[1] * 8
+    out = hash_fixed_folds(t, n_bytes, folds, params, n_strings=folds.size, stride=stride)
+    return out.cpu().numpy().view(np.uint64)
 
 
 def hash_words(words, n_bytes: int, seed, params: HashParams, device=None) -> np.ndarray:

@@ -139,6 +139,27 @@ __device__ __forceinline__ u64 warp_sum(u64 v) {
   return v;
 }
 
+// splitmix seed word idx of a stream keyed by `fold` (hasher.py:55-58)
+__host__ __device__ __forceinline__ u64 splitmix_word(u64 fold, u64 idx) {
+  u64 z = fold + (idx + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Seed words of a job: the shared expanded array (one SeedBuffer for the
+// batch), or -- PERSEED, the many-seeds seam of tests/test_hasher.py:254-310
+// -- recomputed from the string's own fold.
+template <bool PERSEED>
+struct SeedSrc {
+  const u64* S;
+  u64 fold;
+  __device__ __forceinline__ u64 operator()(u64 idx) const {
+    if (PERSEED) return splitmix_word(fold, idx);
+    return __ldg(S + idx);
+  }
+};
+
 // ------------------------------------------------------------ per-string view
 struct Str {
   const uint8_t* p;  // first byte (global)
@@ -149,6 +170,7 @@ struct Str {
   u64 scratch;       // base word of this string's scratch blocks
   u64 cnt;           // base index of this string's counters
   u64 s;             // string index
+  u64 fold;          // PERSEED: this string's seed fold
 };
 
 __host__ __device__ __forceinline__ u32 level_count(u64 n) {
@@ -202,6 +224,7 @@ struct Params {
   const u32* job_str;  // varlen: job -> string
   const u64* meta;     // varlen: 3 u64 per string (job_first, scratch, cnt); entry n = totals
   const u64* S;        // expanded seed words (SeedBuffer.words_np)
+  const u64* folds;    // PERSEED: per-string seed folds
   u64* out;
   u64* scratch;   // level >= job_lvl blocks awaiting their group's merge
   u32* counters;  // per-group arrival counts (self-resetting)
@@ -258,6 +281,7 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u3
     st.cnt = s * P.cnt_per;
   }
   st.s = s;
+  st.fold = P.folds ? P.folds[s] : 0;
   if (!VARLEN && P.frontier_lvl) {  // slice mode: P.n_bytes is the whole string
     jq += (u32)P.slice_job0;
   }

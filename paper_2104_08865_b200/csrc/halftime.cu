@@ -176,7 +176,7 @@ constexpr size_t smem_bytes() {
   constexpr int M = Geo<Var<OUT>>::m;
   constexpr size_t SB = ROUND_INST * M * 8 + 128;
   // ring + mbarriers + level-2/3 accumulators + claimed-job queue, per warp
-  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 2 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8);
+  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 2 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8 + 2 * MAX_EW * 4);
 }
 
 int sm_count(int dev) {
@@ -188,10 +188,10 @@ int sm_count(int dev) {
   return cache[dev];
 }
 
-template <int OUT, bool VARLEN, bool AL8>
+template <int OUT, bool VARLEN, bool AL8, bool PS = false>
 int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   constexpr int W = KCfg<OUT>::W, NS = KCfg<OUT>::NS;
-  auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB, AL8>;
+  auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB, AL8, PS>;
   const size_t smem = smem_bytes<OUT>();
   static std::once_flag once[64];
   int dev = 0;
@@ -263,6 +263,16 @@ int dispatch(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   if (!VARLEN && (reinterpret_cast<uintptr_t>(P.data) % 8) == 0 && P.stride % 8 == 0)
     return dispatch_al<false, true>(out, P, n_jobs_bound, st);
   return dispatch_al<VARLEN, false>(out, P, n_jobs_bound, st);
+}
+// per-string seeds (many-seeds seam)
+int dispatch_ps(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
+  switch (out) {
+    case 16: return launch_hash<16, false, false, true>(P, n_jobs_bound, st);
+    case 24: return launch_hash<24, false, false, true>(P, n_jobs_bound, st);
+    case 32: return launch_hash<32, false, false, true>(P, n_jobs_bound, st);
+    case 40: return launch_hash<40, false, false, true>(P, n_jobs_bound, st);
+  }
+  return fail(HTH_EINVAL, "unsupported output width %d", out);
 }
 
 int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
@@ -518,6 +528,39 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
   set_ctl(P, ws + f.ws_total - 256);
   return dispatch<false>(output_bytes, P, f.n_jobs, st);
+}
+
+int hth_hash_fixed_folds(int output_bytes, const void* d_data, uint64_t n_strings, uint64_t stride_bytes,
+                         uint64_t n_bytes, const uint64_t* d_folds, uint64_t* d_out, void* d_workspace,
+                         uint64_t workspace_bytes, void* stream) {
+  VarInfo v;
+  if (int rc = get_var(output_bytes, &v)) return rc;
+  if (!n_strings) return HTH_OK;
+  if (!d_out || !d_folds) return fail(HTH_EINVAL, "null device pointer");
+  if (n_bytes && !d_data) return fail(HTH_EINVAL, "null data pointer");
+  if (reinterpret_cast<uintptr_t>(d_data) & 15) return fail(HTH_EINVAL, "d_data must be 16-byte aligned");
+  if (n_strings > 1 && stride_bytes && stride_bytes < n_bytes) return fail(HTH_EINVAL, "0 < stride_bytes < n_bytes");
+  const FixedPlan f = fixed_plan(v, n_strings, n_bytes);
+  if (workspace_bytes < f.ws_total) return fail(HTH_EINVAL, "workspace too small");
+  Params P{};
+  P.data = (const uint8_t*)d_data;
+  P.n_strings = n_strings;
+  P.stride = stride_bytes;
+  P.n_bytes = n_bytes;
+  P.J_fixed = f.J;
+  P.n_jobs = f.n_jobs;
+  P.scr_per = f.scr_per;
+  P.cnt_per = f.cnt_per;
+  P.folds = d_folds;
+  P.out = d_out;
+  P.job_lvl = f.job_lvl;
+  uint8_t* ws = (uint8_t*)d_workspace;
+  P.scratch = (u64*)ws;
+  P.acc = (u64*)(ws + f.ws_scratch);
+  P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
+  P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
+  set_ctl(P, ws + f.ws_total - 256);
+  return dispatch_ps(output_bytes, P, f.n_jobs, (cudaStream_t)stream);
 }
 
 int hth_workspace_size_varlen(int output_bytes, uint64_t n_strings, uint64_t total_bytes, uint64_t* bytes) {

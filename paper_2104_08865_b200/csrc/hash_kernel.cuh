@@ -50,10 +50,20 @@ __device__ __forceinline__ u64 mac_coef(int c, u64 acc, u64 h) {
   }
 }
 
+// EHC seed words: constant-bank kernel parameters (one seed for the launch)
+// or, PERSEED, the job's words staged in shared memory.
+template <bool PERSEED>
+struct EhcSrc {
+  const Params& P;
+  const u32* sm;
+  __device__ __forceinline__ u32 lo(int i) const { return PERSEED ? sm[2 * i] : P.ehc[2 * i]; }
+  __device__ __forceinline__ u32 hi(int i) const { return PERSEED ? sm[2 * i + 1] : P.ehc[2 * i + 1]; }
+};
+
 // EHC leaf of instances q and q+4 of the stage, lane j -> CA[r], CB[r]
 // (hasher.py:356-364; ehc.py:102-118).
-template <int OUT, bool AL>
-__device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int j, const Params& P,
+template <int OUT, bool AL, class EH>
+__device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int j, const EH& P,
                                       u64 (&CA)[Var<OUT>::k], u64 (&CB)[Var<OUT>::k]) {
   using V = Var<OUT>;
   constexpr int K = V::k, E = V::e, D = V::d, WB = V::w, M = Geo<V>::m, NP = E - D;
@@ -72,8 +82,8 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
     // hash the systematic items (ehc.py:49-72); seeds are constant-bank operands
 #pragma unroll
     for (int i = 0; i < D; i++) {
-      HA[i] = nh_acc(HA[i], xa[i], P.ehc[2 * (i * WB + u)], P.ehc[2 * (i * WB + u) + 1]);
-      HB[i] = nh_acc(HB[i], xb[i], P.ehc[2 * (i * WB + u)], P.ehc[2 * (i * WB + u) + 1]);
+      HA[i] = nh_acc(HA[i], xa[i], P.lo(i * WB + u), P.hi(i * WB + u));
+      HB[i] = nh_acc(HB[i], xb[i], P.lo(i * WB + u), P.hi(i * WB + u));
     }
     if constexpr (OUT == 16) {
       // XOR parity code (params.py:105-112): one parity item = XOR of all inputs
@@ -83,8 +93,8 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
         pa = pa ^ xa[i];
         pb = pb ^ xb[i];
       }
-      HA[D] = nh_acc(HA[D], pa, P.ehc[2 * (D * WB + u)], P.ehc[2 * (D * WB + u) + 1]);
-      HB[D] = nh_acc(HB[D], pb, P.ehc[2 * (D * WB + u)], P.ehc[2 * (D * WB + u) + 1]);
+      HA[D] = nh_acc(HA[D], pa, P.lo(D * WB + u), P.hi(D * WB + u));
+      HB[D] = nh_acc(HB[D], pb, P.lo(D * WB + u), P.hi(D * WB + u));
     } else {
       // GF(16) Cauchy parity in bit-plane form: plane b of A | plane b of B << 16
       u32 x[4 * D], y[4 * NP];
@@ -100,8 +110,8 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
       for (int p = 0; p < NP; p++) {
         const w2 pa = {__byte_perm(y[4 * p], y[4 * p + 1], 0x5410), __byte_perm(y[4 * p + 2], y[4 * p + 3], 0x5410)};
         const w2 pb = {__byte_perm(y[4 * p], y[4 * p + 1], 0x7632), __byte_perm(y[4 * p + 2], y[4 * p + 3], 0x7632)};
-        HA[D + p] = nh_acc(HA[D + p], pa, P.ehc[2 * ((D + p) * WB + u)], P.ehc[2 * ((D + p) * WB + u) + 1]);
-        HB[D + p] = nh_acc(HB[D + p], pb, P.ehc[2 * ((D + p) * WB + u)], P.ehc[2 * ((D + p) * WB + u) + 1]);
+        HA[D + p] = nh_acc(HA[D + p], pa, P.lo((D + p) * WB + u), P.hi((D + p) * WB + u));
+        HB[D + p] = nh_acc(HB[D + p], pb, P.lo((D + p) * WB + u), P.hi((D + p) * WB + u));
       }
     }
   }
@@ -134,17 +144,16 @@ struct TreeCtx {
 // terms (tree.py:103-134), or it joins a complete group of 8 whose node the
 // last arriving warp computes (nh.py:96-121 with level seeds,
 // tree.py:55-60).  Returns the number of completion events (0 or 1).
-template <int K, int EW>
+template <int K, int EW, class SD>
 __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeCtx<K, EW>& tc, int lvl, u64 idx,
-                                     u64 (&B)[K], u64 (&fin)[K], int lane) {
+                                     u64 (&B)[K], u64 (&fin)[K], int lane, const SD& sd) {
   const int q = lane >> 3, j = lane & 7;
-  const u64* __restrict__ S = P.S;
   for (;;) {
     const u64 len = st.n_inst >> (3 * lvl);
     if (idx >= (len & ~7ull)) {
       if (lane < 8) {
 #pragma unroll
-        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B[r], __ldg(S + tc.F(r) + 56ull * lvl + (idx & 7) * 8 + j));
+        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B[r], sd(tc.F(r) + 56ull * lvl + (idx & 7) * 8 + j));
       }
       return 1;
     }
@@ -181,9 +190,9 @@ __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeC
       const u64 b = __ldcg(g + (q + 4) * 8 * K + r * 8 + j);
       g[q * 8 * K + r * 8 + j] = 0;  // consumed: leave the workspace zeroed
       g[(q + 4) * 8 * K + r * 8 + j] = 0;
-      const u64* s = S + tc.T(r) + 7ull * lvl;
-      u64 v = nh_acc(0, a, __ldg(s + q));
-      v = (q < 3) ? nh_acc(v, b, __ldg(s + q + 4)) : v + b;
+      const u64 s = tc.T(r) + 7ull * lvl;
+      u64 v = nh_acc(0, a, sd(s + q));
+      v = (q < 3) ? nh_acc(v, b, sd(s + q + 4)) : v + b;
       v += shfl_xor(v, 8);
       v += shfl_xor(v, 16);
       B[r] = v;
@@ -195,7 +204,8 @@ __device__ __forceinline__ u32 climb(const Params& P, const Str& st, const TreeC
 
 // AL8: every string starts 8-byte aligned (fixed batches with stride % 8 == 0),
 // so only the aligned-word leaf is compiled in.
-template <int OUT, bool VARLEN, int W, int NS, int MINB, bool AL8>
+// PS: per-string seeds (Params.folds) instead of one shared seed array.
+template <int OUT, bool VARLEN, int W, int NS, int MINB, bool AL8, bool PS>
 __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constant__ Params P) {
   using V = Var<OUT>;
   constexpr int K = V::k, M = Geo<V>::m;
@@ -219,7 +229,7 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
 
   const u64 n_jobs = VARLEN ? P.meta[3 * P.n_strings] : P.n_jobs;
   const int job_lvl = P.job_lvl;
-  const u64* __restrict__ S = P.S;
+  SeedSrc<PS> sd{P.S, 0};
   const u64 pol = policy_evict_first();
 
   // ---- producer: claims jobs dynamically (one atomic per job, lane 0) and
@@ -229,6 +239,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // so dynamic claiming also bounds the tail by one job.
   constexpr u32 QN = NS + 4;
   u64* jq_buf = reinterpret_cast<u64*>(nacc + 2 * K * 8 * W - warp * 2 * K * 8) + warp * QN;
+  // PS: this warp's EHC seed words for the current job, (lo, hi) pairs
+  u32* ehc_sm = reinterpret_cast<u32*>(jq_buf + (W - warp) * QN) + warp * 2 * MAX_EW;
+  const EhcSrc<PS> eh{P, ehc_sm};
   u32 qhead = 0, qtail = 0;        // queue: [qtail, qhead) claimed, not yet started
   bool pdone = false;
   // the first job of every warp is static (job = global warp index), so the
@@ -306,12 +319,22 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     const u32 delta = (u32)(reinterpret_cast<uintptr_t>(st.p) & 15);
     const bool last_job = (jq + 1 == st.J);
     tc.L = st.L;  // tree seeds depend on the layout (hasher.py:130-153) via L only
+    if (PS) {  // this string's own seed stream
+      sd.fold = st.fold;
+      __syncwarp();
+      if (lane < Geo<V>::ew) {
+        const u64 w = splitmix_word(st.fold, lane);
+        ehc_sm[2 * lane] = (u32)w;
+        ehc_sm[2 * lane + 1] = (u32)(w >> 32);
+      }
+      __syncwarp();
+    }
 #if HTH_S1_REGS
-    if (st.L != seedL) {
+    if (PS || st.L != seedL) {
 #pragma unroll
       for (int r = 0; r < K; r++) {
-        s1A[r] = __ldg(S + tc.T(r) + q);
-        s1B[r] = q < 3 ? __ldg(S + tc.T(r) + q + 4) : 0;
+        s1A[r] = sd(tc.T(r) + q);
+        s1B[r] = q < 3 ? sd(tc.T(r) + q + 4) : 0;
       }
       seedL = st.L;
     }
@@ -347,9 +370,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       if (r0 < ninst) {
         u64 CA[K], CB_[K];
         if (!AL8 && (delta & 7))
-          leaf2<OUT, false>(buf, delta, q, j, P, CA, CB_);
+          leaf2<OUT, false>(buf, delta, q, j, eh, CA, CB_);
         else
-          leaf2<OUT, true>(buf, delta, q, j, P, CA, CB_);
+          leaf2<OUT, true>(buf, delta, q, j, eh, CA, CB_);
         const u64 G1 = (inst0 >> 3) + c;  // level-1 group of this round
         if (G1 < len1) {
           // complete group -> level-1 node (nh_tree_node: last block added)
@@ -361,8 +384,8 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
             u64 v = nh_acc(0, CA[r], s1A[r]);
             v = (q < 3) ? nh_acc(v, CB_[r], s1B[r]) : v + CB_[r];
 #else
-            u64 v = nh_acc(0, CA[r], __ldg(S + tc.T(r) + q));
-            v = (q < 3) ? nh_acc(v, CB_[r], __ldg(S + tc.T(r) + q + 4)) : v + CB_[r];
+            u64 v = nh_acc(0, CA[r], sd(tc.T(r) + q));
+            v = (q < 3) ? nh_acc(v, CB_[r], sd(tc.T(r) + q + 4)) : v + CB_[r];
 #endif
             v += shfl_xor(v, 8);
             v += shfl_xor(v, 16);
@@ -372,14 +395,14 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
           if (G1 >= full1) {
             if (q == 0) {  // level-1 leftover -> finalize slot (1, p1)
 #pragma unroll
-              for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B1[r], __ldg(S + tc.F(r) + 56 + p1 * 8 + j));
+              for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B1[r], sd(tc.F(r) + 56 + p1 * 8 + j));
             }
           } else {
             if (q == 0) {
 #pragma unroll
               for (int r = 0; r < K; r++) {
                 const u64 a = nacc[r * 8 + j];
-                nacc[r * 8 + j] = (p1 < 7) ? nh_acc(a, B1[r], __ldg(S + tc.T(r) + 7 + p1)) : a + B1[r];
+                nacc[r * 8 + j] = (p1 < 7) ? nh_acc(a, B1[r], sd(tc.T(r) + 7 + p1)) : a + B1[r];
               }
             }
             __syncwarp();
@@ -392,18 +415,18 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
                 if (lane < 8) nacc[r * 8 + j] = 0;
               }
               if (job_lvl == 2) {
-                events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, B2, fin, lane);
+                events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, B2, fin, lane, sd);
               } else {
                 const int p2 = (int)(G2 & 7);
                 if (lane < 8) {
                   if (G2 >= full2) {
 #pragma unroll
-                    for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B2[r], __ldg(S + tc.F(r) + 112 + p2 * 8 + j));
+                    for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B2[r], sd(tc.F(r) + 112 + p2 * 8 + j));
                   } else {
 #pragma unroll
                     for (int r = 0; r < K; r++) {
                       const u64 a = nacc[(K + r) * 8 + j];
-                      nacc[(K + r) * 8 + j] = (p2 < 7) ? nh_acc(a, B2[r], __ldg(S + tc.T(r) + 14 + p2)) : a + B2[r];
+                      nacc[(K + r) * 8 + j] = (p2 < 7) ? nh_acc(a, B2[r], sd(tc.T(r) + 14 + p2)) : a + B2[r];
                     }
                   }
                 }
@@ -415,7 +438,7 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
                     B3[r] = lane < 8 ? nacc[(K + r) * 8 + j] : 0;
                     if (lane < 8) nacc[(K + r) * 8 + j] = 0;
                   }
-                  events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, B3, fin, lane);
+                  events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, B3, fin, lane, sd);
                 }
               }
             }
@@ -426,8 +449,8 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
           const bool vA = r0 + q < ninst, vB = r0 + q + 4 < ninst;
 #pragma unroll
           for (int r = 0; r < K; r++) {
-            if (vA) fin[r] = nh_acc(fin[r], CA[r], __ldg(S + tc.F(r) + (gA & 7) * 8 + j));
-            if (vB) fin[r] = nh_acc(fin[r], CB_[r], __ldg(S + tc.F(r) + (gB & 7) * 8 + j));
+            if (vA) fin[r] = nh_acc(fin[r], CA[r], sd(tc.F(r) + (gA & 7) * 8 + j));
+            if (vB) fin[r] = nh_acc(fin[r], CB_[r], sd(tc.F(r) + (gB & 7) * 8 + j));
           }
         }
       }
@@ -440,7 +463,7 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
         for (u32 t = lane; t < nt; t += 32) {
           const u64 y = (!AL8 && (delta & 7)) ? ld_word<false>(buf, delta, cw0 + t) : ld_word<true>(buf, delta, cw0 + t);
 #pragma unroll
-          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], y, __ldg(S + tc.R() + r + t));
+          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], y, sd(tc.R() + r + t));
         }
       }
       __syncwarp();
@@ -456,16 +479,16 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
           const u32 l = x / 56u, slot = (x % 56u) >> 3;
           if (slot >= (u32)((st.n_inst >> (3 * l)) & 7)) {
 #pragma unroll
-            for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], 0ull, __ldg(S + tc.F(r) + x));
+            for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], 0ull, sd(tc.F(r) + x));
           }
         }
         if (lane == 0) {
 #pragma unroll
-          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, __ldg(S + tc.F(r) + nz));
+          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, sd(tc.F(r) + nz));
         }
       } else if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, __ldg(S + tc.F(r)));
+        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, sd(tc.F(r)));
       }
     }
     u64 mine = 0;

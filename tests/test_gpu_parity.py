@@ -272,3 +272,62 @@ def test_config5_full_16gib(hh):
     want = coracle.hash_huge(16, host, seed.words_np(0, seed.capacity))
     assert np.array_equal(full, want)
     assert np.array_equal(sliced, want)
+
+
+# ------------------------------------------------------------------ many seeds
+def test_many_seeds_reference_records(hh):
+    # the reference's batched seam with per-row folds (tests/test_hasher.py:254-287 style),
+    # records generated by running the reference (tests/golden/make_golden.py)
+    recs = records("fold")
+    assert len(recs) == 16
+    r0 = recs[0]
+    data = gen_bytes(r0["generator"], r0["length"])
+    words = np.frombuffer(data, dtype="<u8").astype(np.uint64)
+    folds = [r["fold"] for r in recs]
+    got = hh.hash_words_many_seeds(words, r0["length"], folds, hh.variant(r0["variant"]))
+    for r, row in zip(recs, got):
+        assert _hex(row) == r["digest"]
+
+
+@pytest.mark.parametrize("w", VARIANTS)
+def test_many_seeds_vs_oracle(hh, w):
+    import torch
+
+    v = o.variant(w)
+    rng = np.random.default_rng(w + 100)
+    for n in (0, 5, 100, v.m * 8 - 1, v.m * 8 + 3, 9 * v.m * 8 + 17, 70 * v.m * 8 + 5, 600 * v.m * 8 + 1):
+        B = 9
+        folds = rng.integers(0, 1 << 64, size=B, dtype=np.uint64)
+        data = np.frombuffer(o.fill_bytes(max(n, 1), 21), dtype=np.uint8).copy()
+        t = torch.from_numpy(data).cuda()
+        got = _u64(hh.hash_fixed_folds(t, n, folds, hh.variant(w), stride=0))
+        for b in range(B):
+            S = o.splitmix_words(int(folds[b]), 0, o.seed_words_needed(v, n))
+            want = coracle.hash_one(w, data[:n], S)
+            assert np.array_equal(got[b], want), (w, n, b)
+        # distinct inputs too (stride = n rounded to 16)
+        stride = (n + 15) // 16 * 16
+        buf = hh.fill_bytes(B * max(stride, 16), 22)
+        got2 = _u64(hh.hash_fixed_folds(buf, n, folds, hh.variant(w), stride=max(stride, 16)))
+        host = np.frombuffer(o.fill_bytes(B * max(stride, 16), 22), dtype=np.uint8).copy()
+        for b in range(B):
+            S = o.splitmix_words(int(folds[b]), 0, o.seed_words_needed(v, n))
+            s0 = b * max(stride, 16)
+            assert np.array_equal(got2[b], coracle.hash_one(w, host[s0:s0 + n], S)), (w, n, b, "strided")
+
+
+def test_many_seeds_collision_smoke(hh):
+    # GPU-scale version of the reference's seam test (tests/test_hasher.py:263-281):
+    # two 2 KB inputs one byte apart under 10^6 seeds -> no colliding digest
+    import torch
+
+    p = hh.variant(24)
+    n = 2048
+    rng = np.random.default_rng(31)
+    a = rng.integers(0, 1 << 64, size=n // 8, dtype=np.uint64)
+    b = a.copy()
+    b[100] ^= np.uint64(0xFF00000000)
+    folds = rng.integers(0, 1 << 64, size=10 ** 6, dtype=np.uint64)
+    da = hh.hash_fixed_folds(torch.from_numpy(a.view(np.uint8)).cuda(), n, folds, p, stride=0)
+    db = hh.hash_fixed_folds(torch.from_numpy(b.view(np.uint8)).cuda(), n, folds, p, stride=0)
+    assert int(torch.all(da == db, dim=1).sum()) == 0
