@@ -331,3 +331,29 @@ def test_many_seeds_collision_smoke(hh):
     da = hh.hash_fixed_folds(torch.from_numpy(a.view(np.uint8)).cuda(), n, folds, p, stride=0)
     db = hh.hash_fixed_folds(torch.from_numpy(b.view(np.uint8)).cuda(), n, folds, p, stride=0)
     assert int(torch.all(da == db, dim=1).sum()) == 0
+
+
+# ------------------------------------------------------------------ CLI / vector wire format
+def test_cli_vectors_match_reference_grid(hh, tmp_path):
+    from paper_2104_08865_b200.__main__ import main
+
+    path = tmp_path / "vectors.txt"
+    assert main(["vectors", "--emit", str(path)]) == 0
+    ours = [line.strip() for line in open(path) if line.strip()]
+    ref = [r["line"] for r in records("cli_grid")]  # the reference's own vector file (cli.py:189-201)
+    assert ours == ref
+    assert main(["vectors", "--check", str(path)]) == 0
+    path.write_text("\n".join(ours[:-1] + [ours[-1][:-2] + "00"]) + "\n")
+    assert main(["vectors", "--check", str(path)]) == 1
+
+
+def test_cli_hash_empty_stdin(hh, monkeypatch, capsys):
+    # reference CLI golden (pkg/tests/test_cli.py:8, 26-30): 24-byte digest of empty stdin
+    import io
+
+    from paper_2104_08865_b200.__main__ import main
+
+    monkeypatch.setattr("sys.stdin", io.TextIOWrapper(io.BytesIO(b"")))
+    assert main(["hash"]) == 0
+    assert capsys.readouterr().out.strip() == "f76f757856e9c252a8a1ce42dc0e2a5df09d621286a62a2d"
+    assert main(["hash", "--seed-hex", "00"]) == 2
