@@ -221,7 +221,7 @@ struct Params {
   u64 scr_per;   // fixed mode: scratch words per string
   u64 cnt_per;   // fixed mode: counters per string
   const u64* offsets;  // varlen: n_strings + 1 byte offsets
-  const u32* job_str;  // varlen: job -> string
+  const u64* job_map;  // varlen: job -> string | (job index in string) << 32, largest jobs first
   const u64* meta;     // varlen: 3 u64 per string (job_first, scratch, cnt); entry n = totals
   const u64* S;        // expanded seed words (SeedBuffer.words_np)
   const u64* folds;    // PERSEED: per-string seed folds
@@ -262,12 +262,13 @@ template <bool VARLEN, int K, int M>
 __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u32& jq) {
   u64 s;
   if (VARLEN) {
-    s = P.job_str[job];
+    const u64 e = P.job_map[job];
+    s = e & 0xffffffffull;
     const u64 o0 = P.offsets[s], o1 = P.offsets[s + 1];
     st.p = P.data + o0;
     st.n = min(o1 - o0, P.n_bytes);  // clamp to the host-checked bound (plan_count_kernel)
     const u64* mt = P.meta + 3 * s;
-    jq = (u32)(job - mt[0]);
+    jq = (u32)(e >> 32);
     st.scratch = mt[1];
     st.cnt = mt[2];
   } else {

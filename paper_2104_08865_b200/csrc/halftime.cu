@@ -122,8 +122,12 @@ struct TriSum {
   __host__ __device__ Tri operator()(const Tri& x, const Tri& y) const { return {x.a + y.a, x.b + y.b, x.c + y.c}; }
 };
 
+// Varlen plan, pass 1: per string its job count, scratch and counter needs,
+// plus a histogram of job sizes (instances, capped at 64) for LPT ordering.
+constexpr int NCLS = 65;
 template <int OUT>
-__global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, int job_lvl, Tri* tri, int* err) {
+__global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, int job_lvl, Tri* tri, int* err, u32* hist,
+                                  u32* tail_list, u32* tail_count) {
   constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m;
   for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s <= n; s += (u64)gridDim.x * blockDim.x) {
     if (s == n) {
@@ -136,17 +140,51 @@ __global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, int job_lvl,
       nb = max_n;
     }
     const u64 ni = ((nb + 7) >> 3) / M;
+    if (ni == 0) {  // shorter than one instance: tail_varlen_kernel, no job
+      tail_list[atomicAdd(tail_count, 1u)] = (u32)s;
+      tri[s] = {0, 0, 0};
+      continue;
+    }
     const u64 J = job_count(ni, job_lvl);
     u64 w, c;
     scratch_need(ni, K, job_lvl, &w, &c);
     tri[s] = {J, w, c};
+    const u64 per = 1ull << (3 * job_lvl);
+    for (u64 q = 0; q < J; q++) {
+      const u64 jn = ni > q * per ? min(per, ni - q * per) : 0;
+      atomicAdd(hist + (jn > 64 ? 64 : jn), 1u);
+    }
   }
 }
 
-__global__ void plan_fill_kernel(const Tri* meta, u64 n, u32* job_str) {
+// Varlen plan, pass 2: scatter (string, job) pairs into the job map largest
+// job first (counting sort on the size class; order inside a class is
+// arbitrary -- digests do not depend on it).  With dynamic claiming this is
+// longest-processing-time-first scheduling.
+template <int OUT>
+__global__ void plan_scatter_kernel(const u64* off, u64 n, u64 max_n, int job_lvl, const u32* hist, u32* cursor,
+                                    u64* job_map) {
+  constexpr int M = Geo<Var<OUT>>::m;
+  __shared__ u32 base[NCLS];
+  if (threadIdx.x == 0) {
+    u32 acc = 0;
+    for (int c = NCLS - 1; c >= 0; c--) {
+      base[c] = acc;
+      acc += hist[c];
+    }
+  }
+  __syncthreads();
   for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < n; s += (u64)gridDim.x * blockDim.x) {
-    const u64 j0 = meta[s].a, J = meta[s + 1].a - j0;
-    for (u64 q = 0; q < J; q++) job_str[j0 + q] = (u32)s;
+    const u64 nb = min(off[s + 1] - off[s], max_n);
+    const u64 ni = ((nb + 7) >> 3) / M;
+    if (ni == 0) continue;  // handled by tail_varlen_kernel
+    const u64 J = job_count(ni, job_lvl), per = 1ull << (3 * job_lvl);
+    for (u64 q = 0; q < J; q++) {
+      const u64 jn = ni > q * per ? min(per, ni - q * per) : 0;
+      const int c = jn > 64 ? 64 : (int)jn;
+      const u32 pos = base[c] + atomicAdd(cursor + c, 1u);
+      job_map[pos] = s | (q << 32);
+    }
   }
 }
 
@@ -311,7 +349,9 @@ FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
 
 // varlen workspace geometry
 struct VarPlan {
-  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_acc, off_ev, off_ctl, off_cub, cub_bytes, total, max_jobs,
+  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_acc, off_ev, off_ctl, off_hist, off_tail, off_cub,
+      cub_bytes, total,
+      max_jobs,
       scr_words, cnts;
 };
 int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
@@ -328,13 +368,15 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
   p->off_err = o; o += 256;
   p->off_tri = o; o = align_up(o + (n + 1) * sizeof(Tri), 256);
   p->off_meta = o; o = align_up(o + (n + 1) * sizeof(Tri), 256);
-  p->off_jobs = o; o = align_up(o + p->max_jobs * 4, 256);
+  p->off_jobs = o; o = align_up(o + p->max_jobs * 8, 256);
   p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
   // self-resetting state, contiguous so one memset per call clears it
   p->off_cnt = o; o = align_up(o + p->cnts * 4, 256);
   p->off_acc = o; o = align_up(o + n * v.k * 8, 256);
   p->off_ev = o; o = align_up(o + n * 4, 256);
   p->off_ctl = o; o += 256;
+  p->off_hist = o; o = align_up(o + 2 * NCLS * 4 + 4, 256);  // histogram + scatter cursors + tail count
+  p->off_tail = o; o = align_up(o + n * 4, 256);
   p->off_cub = o; o = align_up(o + cub_bytes, 256);
   p->total = o;
   return HTH_OK;
@@ -594,29 +636,37 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   int* err = (int*)(ws + p.off_err);
   Tri* tri = (Tri*)(ws + p.off_tri);
   Tri* meta = (Tri*)(ws + p.off_meta);
-  u32* jobs = (u32*)(ws + p.off_jobs);
+  u64* jobs = (u64*)(ws + p.off_jobs);
+  u32* hist = (u32*)(ws + p.off_hist);
+  u32* tail_count = hist + 2 * NCLS;
+  u32* tail_list = (u32*)(ws + p.off_tail);
   CK(cudaMemsetAsync(err, 0, 4, st));
   // plan areas of an earlier call may overlap this call's counters/accumulators
   CK(cudaMemsetAsync(ws + p.off_cnt, 0, p.off_cub - p.off_cnt, st));
   const u64 blocks = std::min<u64>(ceil_div(n_strings + 1, 256), 4096);
   const int job_lvl = pick_job_lvl(((max_n_bytes + 7) / 8) / (u64)v.m);
   switch (output_bytes) {
-    case 16: plan_count_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
-    case 24: plan_count_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
-    case 32: plan_count_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
-    case 40: plan_count_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err); break;
+    case 16: plan_count_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
+    case 24: plan_count_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
+    case 32: plan_count_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
+    case 40: plan_count_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
   }
   CK(cudaGetLastError());
   size_t cub_bytes = p.cub_bytes;
   CK(cub::DeviceScan::ExclusiveScan(ws + p.off_cub, cub_bytes, tri, meta, TriSum(), Tri{0, 0, 0},
                                     (int64_t)(n_strings + 1), st));
-  plan_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(meta, n_strings, jobs);
+  switch (output_bytes) {
+    case 16: plan_scatter_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
+    case 24: plan_scatter_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
+    case 32: plan_scatter_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
+    case 40: plan_scatter_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
+  }
   CK(cudaGetLastError());
   Params P{};
   P.data = (const uint8_t*)d_data;
   P.n_strings = n_strings;
   P.offsets = d_offsets;
-  P.job_str = jobs;
+  P.job_map = jobs;
   P.meta = (const u64*)meta;
   P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_count)
   P.S = d_seed;
@@ -628,6 +678,29 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   P.acc = (u64*)(ws + p.off_acc);
   P.events = (u32*)(ws + p.off_ev);
   set_ctl(P, ws + p.off_ctl);
+  {
+    TailVarParams T{};
+    T.data = (const uint8_t*)d_data;
+    T.offsets = d_offsets;
+    T.list = tail_list;
+    T.count = tail_count;
+    T.max_n = max_n_bytes;
+    T.S = d_seed;
+    T.R = (u64)v.ew + 71ull * v.k;  // L' = 1 layout (hasher.py:130-153)
+    T.F0 = (u64)v.ew + 7ull * v.k;
+    T.Fstep = 64;
+    T.out = d_out;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const unsigned tb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 16), (u64)sm_count(dev) * 8));
+    switch (output_bytes) {
+      case 16: tail_varlen_kernel<16><<<tb, 256, 0, st>>>(T); break;
+      case 24: tail_varlen_kernel<24><<<tb, 256, 0, st>>>(T); break;
+      case 32: tail_varlen_kernel<32><<<tb, 256, 0, st>>>(T); break;
+      case 40: tail_varlen_kernel<40><<<tb, 256, 0, st>>>(T); break;
+    }
+    CK(cudaGetLastError());
+  }
   return dispatch<true>(output_bytes, P, p.max_jobs, st);
 }
 
