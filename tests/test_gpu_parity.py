@@ -357,3 +357,106 @@ def test_cli_hash_empty_stdin(hh, monkeypatch, capsys):
     assert main(["hash"]) == 0
     assert capsys.readouterr().out.strip() == "f76f757856e9c252a8a1ce42dc0e2a5df09d621286a62a2d"
     assert main(["hash", "--seed-hex", "00"]) == 2
+
+
+# ------------------------------------------------------------------ edge cases
+def test_empty_batches_and_zero_length(hh):
+    import torch
+
+    p = hh.variant(32)
+    seed = hh.seed_for_input(b"\0" * 32, p, 0)
+    buf = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    out = hh.hash_fixed(buf, 0, seed, p, n_strings=0, stride=16)
+    assert out.shape == (0, 4)
+    out = hh.hash_fixed(buf, 0, seed, p, n_strings=5, stride=0)  # five empty strings
+    want = o.hash_batch(o.variant(32), np.zeros((1, 0), np.uint64), 0, seed.words_np(0, seed.capacity))[0]
+    assert all(np.array_equal(row, want) for row in _u64(out))
+    got = hh.hash_varlen(buf, np.array([0, 0, 0], dtype=np.uint64), seed, p)
+    assert all(np.array_equal(row, want) for row in _u64(got))
+
+
+def test_varlen_mixed_huge_and_tiny(hh):
+    # multi-level merges (level >= 3 scratch) next to tail-only strings in one varlen call
+    w = 24
+    v = o.variant(w)
+    lengths = np.array([0, 3, 5000, 600 * v.m * 8 + 7, 1, 70 * v.m * 8, 4097 * v.m * 8 + 13, 100, 64 * v.m * 8],
+                       dtype=np.int64)
+    from workloads import offsets_of
+
+    off = offsets_of(lengths) + np.uint64(5)  # unaligned base offset for every string
+    total = int(off[-1])
+    buf = hh.fill_bytes(total, 31)
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, int(lengths.max()))
+    got = _u64(hh.hash_varlen(buf, off, seed, p))
+    host = np.frombuffer(o.fill_bytes(total, 31), dtype=np.uint8).copy()
+    want = coracle.hash_varlen(w, host, off, seed.words_np(0, seed.capacity))
+    assert np.array_equal(got, want)
+
+
+def test_varlen_bound_violation_is_flagged(hh):
+    import ctypes
+
+    import torch
+
+    from paper_2104_08865_b200 import _lib, batch
+
+    p = hh.variant(16)
+    off = np.array([0, 100, 7000], dtype=np.uint64)  # string 1: 9 instances -> 2 levels
+    buf = hh.fill_bytes(7000, 2)
+    seed = hh.seed_for_input(b"\0" * 32, p, 7000)
+    with pytest.raises(hh.SeedSizeError):  # host-side bound check against capacity
+        hh.hash_varlen(buf, off, hh.seed_for_input(b"\0" * 32, p, 10), p)
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    out = torch.empty((2, 2), dtype=torch.int64, device="cuda")
+    ws = torch.zeros(batch.workspace_varlen(p, 2, 7000), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    L = _lib.lib()
+    rc = L.hth_hash_varlen(16, buf.data_ptr(), d_off.data_ptr(), 2, 200, 7000, seed.fold,
+                           seed.device_words().data_ptr(), seed.capacity, out.data_ptr(), ws.data_ptr(),
+                           ws.numel(), st)
+    assert rc == 0
+    assert L.hth_varlen_status(ws.data_ptr(), st) == _lib.HTH_ESEEDSIZE  # string 1 exceeds max_n_bytes
+    rc = L.hth_hash_varlen(16, buf.data_ptr(), d_off.data_ptr(), 2, 7000, 7000, seed.fold,
+                           seed.device_words().data_ptr(), seed.capacity, out.data_ptr(), ws.data_ptr(),
+                           ws.numel(), st)
+    assert rc == 0 and L.hth_varlen_status(ws.data_ptr(), st) == 0
+
+
+def test_concurrent_streams(hh):
+    # independent calls on two streams with their own workspaces give the same digests
+    import torch
+
+    from paper_2104_08865_b200 import batch
+
+    w = 40
+    v = o.variant(w)
+    n = 1100 * v.m * 8 + 9
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, n)
+    bufs = [hh.fill_bytes(4 * n, 40 + i) for i in range(2)]
+    seed.device_words()
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i, stv in enumerate(streams):
+        with torch.cuda.stream(stv):
+            ws = torch.zeros(batch.workspace_fixed(p, 4, n), dtype=torch.uint8, device="cuda")
+            outs.append(hh.hash_fixed(bufs[i], n, seed, p, n_strings=4, stride=n, workspace=ws))
+    torch.cuda.synchronize()
+    for i in range(2):
+        host = np.frombuffer(o.fill_bytes(4 * n, 40 + i), dtype=np.uint8).copy()
+        want = coracle.hash_fixed(w, host, 4, n, n, seed.words_np(0, seed.capacity))
+        assert np.array_equal(_u64(outs[i]), want)
+
+
+def test_host_api_strides_and_capacity(hh):
+    p = hh.variant(16)
+    n, B, stride = 3001, 21, 3013  # unaligned stride on the host
+    host = np.frombuffer(o.fill_bytes(B * stride, 8), dtype=np.uint8).copy()
+    got = hh.hash_fixed_host(host, B, n, bytes(range(32)), p, stride=stride)
+    S = o.splitmix_words(o.master_fold(bytes(range(32))), 0, o.seed_words_needed(o.variant(16), n))
+    want = coracle.hash_fixed(16, host, B, stride, n, S)
+    assert np.array_equal(got, want)
+    with pytest.raises(hh.SeedSizeError):
+        hh.hash_fixed_host(host, B, n, bytes(range(32)), p, stride=stride, seed_capacity=5)
