@@ -196,7 +196,7 @@ def setup_fixed(hh, torch, workload, rank=0, world=1):
     return dict(p=p, buf=buf, seed=seed, out=out, B=B, n=n, w=w)
 
 
-def run_fixed(hh, torch, ctx, steps, warmup, flush=None):
+def run_fixed(hh, torch, ctx, steps, warmup, flush=None, barrier=None):
     p, buf, seed, out, B, n = ctx["p"], ctx["buf"], ctx["seed"], ctx["out"], ctx["B"], ctx["n"]
     stream = torch.cuda.current_stream()
 
@@ -206,6 +206,9 @@ def run_fixed(hh, torch, ctx, steps, warmup, flush=None):
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
+    if barrier:
+        barrier()
+        torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -219,6 +222,8 @@ def run_fixed(hh, torch, ctx, steps, warmup, flush=None):
         evs[i][1].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
+    if barrier:
+        barrier()
     wall1 = time.time()
     per = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(per) if flush is not None else t_start.elapsed_time(t_end)
@@ -379,13 +384,9 @@ def arm_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    total_ms, per, (w0, w1) = run_fixed(hh, torch, ctx, args.steps, args.warmup)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    # warm-up, then barrier + synchronize on both sides of exactly K timed steps
+    total_ms, per, (w0, w1) = run_fixed(hh, torch, ctx, args.steps, args.warmup,
+                                        barrier=dist.barrier if dist else None)
     time.sleep(0.2)
     sampler.stop()
     clocks = sampler.summary(w0, w1)
@@ -446,7 +447,7 @@ def arm_ours(args, rank, world, local_rank):
                        "parallelism": f"dp{world} (independent strings, no collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(workload),
-                         "kernel": "hash_kernel<40,false,W=2,NS=2,MINB=4>", "kernel_ms": kernel_ms,
+                         "kernel": "hash_kernel<40, fixed, W=2, NS=2, MINB=6, AL8> (one launch per step)", "kernel_ms": kernel_ms,
                          "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
