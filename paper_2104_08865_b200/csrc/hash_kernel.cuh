@@ -14,13 +14,16 @@ namespace hth {
 
 // Little-endian u64 word `widx` of a stage whose first string byte sits at
 // smem offset `delta` (0..15).  AL: delta % 8 == 0 (aligned LDS.64).
+// Unaligned: three 32-bit shared loads and two funnel shifts (SHF.R.W) for
+// any byte offset (a shift of 0 passes the first operand through).
 template <bool AL>
 __device__ __forceinline__ u64 ld_word(const uint8_t* buf, u32 delta, u32 widx) {
   if (AL) return *reinterpret_cast<const u64*>(buf + delta + widx * 8u);
   const u32 off = delta + widx * 8u;
-  const u64* p = reinterpret_cast<const u64*>(buf + (off & ~7u));
-  const u32 sh = (off & 7u) * 8u;
-  return (p[0] >> sh) | (p[1] << (64u - sh));
+  const u32* p = reinterpret_cast<const u32*>(buf + (off & ~3u));
+  const u32 sh = (off & 3u) * 8u;
+  const u32 lo = __funnelshift_r(p[0], p[1], sh), hi = __funnelshift_r(p[1], p[2], sh);
+  return ((u64)hi << 32) | lo;
 }
 
 template <int OUT>
