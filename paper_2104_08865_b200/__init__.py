@@ -30,7 +30,7 @@ __all__ = [
     "Digest", "ErasureCode", "HashParams", "SeedBuffer", "SeedLayout", "SeedSizeError", "TransformMatrix",
     "VARIANTS", "digest", "expand_seed", "hash_bytes", "instance_count", "seed_for_input", "seed_layout",
     "seed_words_needed", "variant", "hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes",
-    "hash_fixed_folds", "hash_words_many_seeds",
+    "hash_fixed_folds", "hash_words_many_seeds", "StreamHasher",
     "__version__",
 ]
 
@@ -42,4 +42,8 @@ def __getattr__(name):
         from . import batch
 
         return getattr(batch, name)
+    if name == "StreamHasher":
+        from .stream import StreamHasher
+
+        return StreamHasher
     raise AttributeError(name)

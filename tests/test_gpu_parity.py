@@ -460,3 +460,37 @@ def test_host_api_strides_and_capacity(hh):
     assert np.array_equal(got, want)
     with pytest.raises(hh.SeedSizeError):
         hh.hash_fixed_host(host, B, n, bytes(range(32)), p, stride=stride, seed_capacity=5)
+
+
+# ------------------------------------------------------------------ streaming
+@pytest.mark.parametrize("w", (16, 40))
+def test_stream_hasher_matches_one_shot(hh, w):
+    import torch
+
+    from paper_2104_08865_b200.stream import StreamHasher
+
+    v = o.variant(w)
+    ib = v.m * 8
+    rng = np.random.default_rng(w)
+    p = hh.variant(w)
+    for inst, extra in ((0, 0), (0, 77), (100, 5), (511, 0), (512, 0), (512, 9), (1024, 0), (1024, 3),
+                        (3 * 512 + 17, 41), (5000, 1)):
+        n = inst * ib + extra
+        data = o.fill_bytes(n, 55)
+        seed = hh.seed_for_input(bytes(range(32)), p, n)
+        want = hh.hash_bytes(data, seed, p)
+        for trial in range(2):
+            h = StreamHasher(p, seed, n, slice_bytes=512 * ib)  # c = 3: slices of 512 instances
+            pos = 0
+            while pos < n:
+                step = int(rng.integers(1, max(2, n // 3)))
+                chunk = data[pos:pos + step]
+                h.update(torch.frombuffer(bytearray(chunk), dtype=torch.uint8).cuda() if trial else chunk)
+                pos += len(chunk)
+            assert h.digest() == want, (w, inst, extra, trial)
+    h = StreamHasher(p, hh.seed_for_input(b"\0" * 32, p, 10), 10)
+    h.update(b"12345")
+    with pytest.raises(ValueError):
+        h.digest()
+    with pytest.raises(ValueError):
+        h.update(b"123456")
