@@ -232,6 +232,10 @@ struct Params {
   u32* events;    // per multi-job string: completion events seen (self-resetting)
   unsigned long long* job_ctr;  // dynamic job claiming (self-resetting)
   u32* exit_ctr;                 // warps finished (self-resetting)
+  // fixed-length batches: the zero-slot and length-tag finalize terms
+  // (tree.py:103-134) depend only on (n, seed), so the host sums them once
+  int fin_const_ok;
+  u64 fin_const[5];
   int job_lvl;    // a warp job is one level-`job_lvl` subtree
   // slice mode (one string split across GPUs, fixed mode with n_strings = 1):
   // jobs cover global instances [slice_inst0, ...); finished non-leftover

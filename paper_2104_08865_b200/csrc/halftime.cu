@@ -85,6 +85,31 @@ void set_ctl(Params& P, uint8_t* ctl) {
   P.exit_ctr = reinterpret_cast<u32*>(ctl + 8);
 }
 
+// Zero-slot + length-tag finalize terms of one string length, summed on the
+// host (tree.py:103-134, hasher.py:387-405): identical for every string of a
+// fixed-length batch, so the kernel just adds them.
+void fill_fin_const(const VarInfo& v, u64 fold, u64 n_bytes, Params& P) {
+  const Layout l = make_layout(v, n_bytes);
+  auto nh = [](u64 x, u64 s) { return (u64)((u32)x + (u32)s) * (u64)((u32)(x >> 32) + (u32)(s >> 32)); };
+  auto S = [&](u64 i) { return host_mix(fold + (i + 1) * 0x9E3779B97F4A7C15ull); };
+  for (int r = 0; r < v.k; r++) {
+    const u64 F = l.fin_start + l.fin_per * r;
+    u64 acc = 0;
+    if (l.n_inst) {
+      for (u64 lv = 0; lv < l.levels; lv++) {
+        const u64 digit = (l.n_inst >> (3 * lv)) & 7;
+        for (u64 slot = digit; slot < 7; slot++)
+          for (u64 j = 0; j < 8; j++) acc += nh(0, S(F + 56 * lv + 8 * slot + j));
+      }
+      acc += nh(n_bytes, S(F + 56 * l.levels));
+    } else {
+      acc += nh(n_bytes, S(F));
+    }
+    P.fin_const[r] = acc;
+  }
+  P.fin_const_ok = 1;
+}
+
 u64 fold_of(const uint8_t* m) {
   u64 w[4];
   memcpy(w, m, 32);
@@ -540,6 +565,7 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.out = d_out;
   P.job_lvl = f.job_lvl;
   fill_ehc(v, seed_fold, P);
+  fill_fin_const(v, seed_fold, n_bytes, P);
   if (f.n_inst == 0 && n_bytes > 0 && stride_bytes % 16 == 0 && stride_bytes <= 2048) {
     // strings shorter than one instance: dedicated half-warp-per-string kernel
     TailParams T{};
@@ -778,6 +804,7 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   P.frontier_base = inst_begin >> (3 * frontier_level);
   P.frontier = d_frontier;
   fill_ehc(v, seed_fold, P);
+  fill_fin_const(v, seed_fold, n_bytes, P);
   uint8_t* ws = (uint8_t*)d_workspace;
   P.scratch = (u64*)ws;
   P.acc = d_partial;

@@ -474,7 +474,12 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       p_issue();
     }
 
-    if (last_job) {
+    if (last_job && P.fin_const_ok) {
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < K; r++) fin[r] += P.fin_const[r];
+      }
+    } else if (last_job) {
       // zero slots and the length tag of the finalize NH (hasher.py:387-405)
       if (st.n_inst) {
         const u32 nz = 56u * st.L;
