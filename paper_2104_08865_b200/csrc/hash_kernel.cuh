@@ -253,50 +253,54 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // small batches (one job per warp at most) never touch the counters
   const bool claims = n_jobs > n_warps;
   bool first = HTH_STATIC_FIRST || !claims;
-  u32 pchunk = 0, pnchunks = 0, pseq = 0, cseq = 0;
-  const uint8_t* pbase = nullptr;
-  u64 pbytes = 0;
+  u32 pseq = 0, cseq = 0;
+  u64 psrc = 0;  // next chunk's first byte (global address)
+  u64 prem = 0;  // bytes of the current producer job not yet issued
+  // cold path: claim the next job and set up its byte range (once per job)
+  auto p_claim = [&]() -> bool {
+    if (pdone || qhead - qtail >= QN) return false;
+    unsigned long long jc = (u64)blockIdx.x * W + warp;
+    if (!first) {
+      if (!claims) {
+        pdone = true;
+        return false;
+      }
+      if (lane == 0) jc = (HTH_STATIC_FIRST ? n_warps : 0) + atomicAdd(P.job_ctr, 1ull);
+      jc = __shfl_sync(0xffffffffu, jc, 0);
+    }
+    first = false;
+    if (jc >= n_jobs) {
+      pdone = true;
+      return false;
+    }
+    if (lane == 0) jq_buf[qhead % QN] = jc;
+    qhead++;
+    Str st;
+    u32 jq, ni;
+    u64 b0;
+    decode_job<VARLEN, K, M>(P, jc, st, jq);
+    job_span<M>(st, jq, job_lvl, b0, prem, ni);
+    psrc = reinterpret_cast<u64>(st.p) + b0;
+    return true;
+  };
+  // hot path: one bulk copy per round, address advanced incrementally
   auto p_issue = [&]() {
     while (pseq - cseq < (u32)NS) {
-      if (pchunk >= pnchunks) {  // current producer job fully issued: claim the next
-        if (pdone || qhead - qtail >= QN) return;
-        unsigned long long jc = (u64)blockIdx.x * W + warp;
-        if (!first) {
-          if (!claims) {
-            pdone = true;
-            return;
-          }
-          if (lane == 0) jc = (HTH_STATIC_FIRST ? n_warps : 0) + atomicAdd(P.job_ctr, 1ull);
-          jc = __shfl_sync(0xffffffffu, jc, 0);
-        }
-        first = false;
-        if (jc >= n_jobs) {
-          pdone = true;
-          return;
-        }
-        if (lane == 0) jq_buf[qhead % QN] = jc;
-        qhead++;
-        Str st;
-        u32 jq, ni;
-        u64 b0;
-        decode_job<VARLEN, K, M>(P, jc, st, jq);
-        job_span<M>(st, jq, job_lvl, b0, pbytes, ni);
-        pbase = st.p + b0;
-        pnchunks = (u32)ceil_div(pbytes, CB);
-        pchunk = 0;
+      if (prem == 0) {
+        if (!p_claim()) return;
         continue;
       }
+      const u32 len = (u32)min((u64)CB, prem);
+      const u64 a0 = psrc & ~15ull;
+      const u32 bytes = (u32)(((psrc + len + 15) & ~15ull) - a0);
       const u32 slot = pseq % NS;
-      const uint8_t* src = pbase + (u64)pchunk * CB;
-      const u64 len = min((u64)CB, pbytes - (u64)pchunk * CB);
-      const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
-      const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src) + len + 15) & ~uintptr_t(15);
       if (lane == 0) {
-        mbar_arrive_expect_tx(&bars[slot], (u32)(a1 - a0));
-        bulk_g2s(ring + slot * SB, reinterpret_cast<const void*>(a0), (u32)(a1 - a0), &bars[slot], pol);
+        mbar_arrive_expect_tx(&bars[slot], bytes);
+        bulk_g2s(ring + slot * SB, reinterpret_cast<const void*>(a0), bytes, &bars[slot], pol);
       }
       pseq++;
-      pchunk++;
+      psrc += CB;
+      prem -= len;
     }
   };
   p_issue();

@@ -27,11 +27,7 @@ def test_schedule_matches_reference_encode(w):
     v = o.variant(w)
     d, P = gen.VARIANTS[w]
     assert [list(r) for r in v.parity] == P
-    rows = []
-    for p in range(len(P)):
-        for a in range(4):
-            rows.append({i * 4 + b for i, c in enumerate(P[p]) for b in range(4) if gen.mulmat(c)[a][b]})
-    temps, red = gen.paar(rows, 4 * d)
+    prog = gen.lop3_program(d, P)  # exactly what encode_gen.cuh computes
     rng = np.random.default_rng(w)
     for _ in range(200):
         xa = rng.integers(0, 1 << 64, size=d, dtype=np.uint64)
@@ -40,12 +36,15 @@ def test_schedule_matches_reference_encode(w):
         for i in range(d):
             for b, pl in enumerate(planes(xa[i], xb[i])):
                 vals[4 * i + b] = pl
-        for t, a, b in temps:
-            vals[t] = vals[a] ^ vals[b]
-        y = [0] * len(red)
-        for k, r in enumerate(red):
-            for t in r:
-                y[k] ^= vals[t]
+        y = [0] * (4 * len(P))
+        for dest, terms in prog:
+            acc = 0
+            for t in terms:
+                acc ^= vals[int(t[1:]) if isinstance(t, str) else t]
+            if dest.startswith("t"):
+                vals[int(dest[1:])] = acc
+            else:
+                y[int(dest[2:-1])] = acc
         for p, row in enumerate(v.parity):
             want_a = np.uint64(0)
             want_b = np.uint64(0)
