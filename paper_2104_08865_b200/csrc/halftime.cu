@@ -234,12 +234,14 @@ template <> struct KCfg<32> { static constexpr int W = 2, NS = 2, MINB = HTH_V24
 #endif
 template <> struct KCfg<40> { static constexpr int W = HTH_V40_W, NS = HTH_V40_NS, MINB = HTH_V40_MINB; };
 
-template <int OUT>
+template <int OUT, bool PS = false>
 constexpr size_t smem_bytes() {
   constexpr int M = Geo<Var<OUT>>::m;
-  constexpr size_t SB = ROUND_INST * M * 8 + 128;
-  // ring + mbarriers + level-2/3 accumulators + claimed-job queue, per warp
-  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 2 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8 + 2 * MAX_EW * 4);
+  constexpr size_t SB = ROUND_INST * M * 8 + 32;
+  // ring + mbarriers + parked level-1 group and level-3 accumulator +
+  // claimed-job queue (+ per-job EHC seeds in many-seeds mode), per warp
+  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 9 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8 +
+                         (PS ? 2 * MAX_EW * 4 : 0));
 }
 
 int sm_count(int dev) {
@@ -255,7 +257,7 @@ template <int OUT, bool VARLEN, bool AL8, bool PS = false>
 int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   constexpr int W = KCfg<OUT>::W, NS = KCfg<OUT>::NS;
   auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB, AL8, PS>;
-  const size_t smem = smem_bytes<OUT>();
+  const size_t smem = smem_bytes<OUT, PS>();
   static std::once_flag once[64];
   int dev = 0;
   CK(cudaGetDevice(&dev));

@@ -213,16 +213,18 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   using V = Var<OUT>;
   constexpr int K = V::k, M = Geo<V>::m;
   constexpr u32 CB = ROUND_INST * M * 8;  // stage payload bytes
-  constexpr u32 SB = CB + 128;            // stage buffer (alignment + overread slack)
+  constexpr u32 SB = CB + 32;             // stage buffer: 16-B alignment superset + unaligned overread
   extern __shared__ __align__(128) uint8_t smem[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = lane >> 3, j = lane & 7;
   uint8_t* ring = smem + warp * NS * SB;
   u64* bars = reinterpret_cast<u64*>(smem + W * NS * SB) + warp * NS;
-  // level-2 / level-3 node accumulators of this warp, [level][r][lane 0..7];
-  // touched once per round at most, so they live in shared memory, not registers
-  u64* nacc = reinterpret_cast<u64*>(smem + W * NS * SB + W * NS * 8) + warp * 2 * K * 8;
+  // per warp: the 8 level-1 blocks of the current level-2 group, [pos][r][lane],
+  // then the level-3 node accumulator [r][lane] -- shared memory, not registers
+  constexpr int NACC = 9 * K * 8;
+  u64* nacc = reinterpret_cast<u64*>(smem + W * NS * SB + W * NS * 8) + warp * NACC;
+  u64* n3acc = nacc + 8 * K * 8;
   if (lane == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // Jobs are claimed in index order: fixed mode is jq-major (full jobs first),
   // so dynamic claiming also bounds the tail by one job.
   constexpr u32 QN = NS + 4;
-  u64* jq_buf = reinterpret_cast<u64*>(nacc + 2 * K * 8 * W - warp * 2 * K * 8) + warp * QN;
+  u64* jq_buf = reinterpret_cast<u64*>(smem + W * NS * SB + W * NS * 8) + W * NACC + warp * QN;
   // PS: this warp's EHC seed words for the current job, (lo, hi) pairs
   u32* ehc_sm = reinterpret_cast<u32*>(jq_buf + (W - warp) * QN) + warp * 2 * MAX_EW;
   const EhcSrc<PS> eh{P, ehc_sm};
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     for (int r = 0; r < K; r++) fin[r] = 0;
     if (lane < 8) {
 #pragma unroll
-      for (int r = 0; r < 2 * K; r++) nacc[r * 8 + lane] = 0;
+      for (int r = 0; r < K; r++) n3acc[r * 8 + lane] = 0;
     }
     const u64 inst0 = (u64)jq << (3 * job_lvl);
     const u64 full0 = st.n_inst & ~7ull;  // instances in complete level-1 groups
@@ -405,22 +407,26 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
               for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B1[r], sd(tc.F(r) + 56 + p1 * 8 + j));
             }
           } else {
+            // park the level-1 block (lanes 0-7); every 8th round all 32 lanes
+            // form the level-2 node from the parked group
             if (q == 0) {
 #pragma unroll
-              for (int r = 0; r < K; r++) {
-                const u64 a = nacc[r * 8 + j];
-                nacc[r * 8 + j] = (p1 < 7) ? nh_acc(a, B1[r], sd(tc.T(r) + 7 + p1)) : a + B1[r];
-              }
+              for (int r = 0; r < K; r++) nacc[(p1 * K + r) * 8 + j] = B1[r];
             }
-            __syncwarp();
             if (p1 == 7) {
-              const u64 G2 = G1 >> 3;  // level-2 block complete (lanes 0-7)
+              __syncwarp();
+              const u64 G2 = G1 >> 3;  // level-2 block complete (replicated in all lanes)
               u64 B2[K];
 #pragma unroll
               for (int r = 0; r < K; r++) {
-                B2[r] = lane < 8 ? nacc[r * 8 + j] : 0;
-                if (lane < 8) nacc[r * 8 + j] = 0;
+                const u64 a = nacc[(q * K + r) * 8 + j], b = nacc[((q + 4) * K + r) * 8 + j];
+                u64 v = nh_acc(0, a, sd(tc.T(r) + 7 + q));
+                v = (q < 3) ? nh_acc(v, b, sd(tc.T(r) + 11 + q)) : v + b;
+                v += shfl_xor(v, 8);
+                v += shfl_xor(v, 16);
+                B2[r] = v;
               }
+              __syncwarp();
               if (job_lvl == 2) {
                 events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, B2, fin, lane, sd);
               } else {
@@ -432,8 +438,8 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
                   } else {
 #pragma unroll
                     for (int r = 0; r < K; r++) {
-                      const u64 a = nacc[(K + r) * 8 + j];
-                      nacc[(K + r) * 8 + j] = (p2 < 7) ? nh_acc(a, B2[r], sd(tc.T(r) + 14 + p2)) : a + B2[r];
+                      const u64 a = n3acc[r * 8 + j];
+                      n3acc[r * 8 + j] = (p2 < 7) ? nh_acc(a, B2[r], sd(tc.T(r) + 14 + p2)) : a + B2[r];
                     }
                   }
                 }
@@ -442,8 +448,8 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
                   u64 B3[K];
 #pragma unroll
                   for (int r = 0; r < K; r++) {
-                    B3[r] = lane < 8 ? nacc[(K + r) * 8 + j] : 0;
-                    if (lane < 8) nacc[(K + r) * 8 + j] = 0;
+                    B3[r] = lane < 8 ? n3acc[r * 8 + j] : 0;
+                    if (lane < 8) n3acc[r * 8 + j] = 0;
                   }
                   events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, B3, fin, lane, sd);
                 }
