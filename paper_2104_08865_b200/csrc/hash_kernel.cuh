@@ -118,14 +118,24 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
       }
     }
   }
-  // combine (ehc.py:75-99)
+  // combine (ehc.py:75-99): the coefficient-1 terms as one plain sum (3-input
+  // IADD3 pairs), then the other coefficients as IMAD.WIDE/IMAD chains
 #pragma unroll
   for (int r = 0; r < K; r++) {
     u64 a = 0, b = 0;
 #pragma unroll
     for (int i = 0; i < E; i++) {
-      a = mac_coef(V::mat(r, i), a, HA[i]);
-      b = mac_coef(V::mat(r, i), b, HB[i]);
+      if (V::mat(r, i) == 1) {
+        a += HA[i];
+        b += HB[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      if (V::mat(r, i) > 1) {
+        a = mac_coef(V::mat(r, i), a, HA[i]);
+        b = mac_coef(V::mat(r, i), b, HB[i]);
+      }
     }
     CA[r] = a;
     CB[r] = b;
