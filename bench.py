@@ -475,7 +475,7 @@ def arm_ours(args, rank, world, local_rank):
                        "parallelism": f"dp{world} (independent strings, no collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(workload),
-                         "kernel": "hash_kernel<40, fixed, W=2, NS=2, MINB=6, AL8> (one launch per step)", "kernel_ms": kernel_ms,
+                         "kernel": "hash_kernel<40, fixed, W=2, NS=2, MINB=5, AL8> (one launch per step)", "kernel_ms": kernel_ms,
                          "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,

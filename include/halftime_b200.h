@@ -119,7 +119,8 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
                     uint64_t seed_capacity, uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes,
                     void* stream);
 /* Synchronizes `stream`; returns HTH_ESEEDSIZE if the last varlen call on this
- * workspace met a string longer than its max_n_bytes, else HTH_OK. */
+ * workspace met a string longer than its max_n_bytes, HTH_EINVAL if the
+ * strings held more bytes than its total_bytes declared, else HTH_OK. */
 int hth_varlen_status(void* d_workspace, void* stream);
 
 /* ---- one string split across devices (config 5): the reference's stack

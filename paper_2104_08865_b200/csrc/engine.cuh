@@ -211,6 +211,14 @@ __host__ __device__ __forceinline__ u32 string_events(u64 n_inst, int job_lvl) {
   return e;
 }
 
+// Varlen jobs are bucketed by size class c = min(instances, 64) into queues
+// of fixed capacity: a class-c job holds >= c instances, so at most
+// q_inst / c of them exist.  Claim order is largest class first (LPT).
+constexpr int NCLS = 65;
+__host__ __device__ __forceinline__ u64 queue_cap(int c, u64 max_jobs, u64 q_inst) {
+  return c == 0 ? 0 : min(max_jobs, q_inst / (u64)c + 1);
+}
+
 struct Params {
   const uint8_t* data;
   u64 n_strings;
@@ -221,8 +229,9 @@ struct Params {
   u64 scr_per;   // fixed mode: scratch words per string
   u64 cnt_per;   // fixed mode: counters per string
   const u64* offsets;  // varlen: n_strings + 1 byte offsets
-  const u64* job_map;  // varlen: job -> string | (job index in string) << 32, largest jobs first
-  const u64* meta;     // varlen: 3 u64 per string (job_first, scratch, cnt); entry n = totals
+  const u64* job_map;  // varlen: per-size-class job queues of (string | job index in string << 32)
+  const u64* meta;     // varlen: 2 u64 per string (scratch, counter bases; multi-job strings)
+  const u32* cls_cnt;  // varlen: jobs per size class (plan_queue_kernel)
   const u64* S;        // expanded seed words (SeedBuffer.words_np)
   const u64* folds;    // PERSEED: per-string seed folds
   u64* out;
@@ -250,6 +259,8 @@ struct Params {
   // a __grid_constant__, so these are constant-bank operands of the NH adds.
   // Interleaved (lo, hi) so one 64-bit constant load fetches both halves.
   alignas(8) u32 ehc[2 * MAX_EW];
+  // varlen: start of each size class's queue in job_map (host-computed; [NCLS] = end)
+  u64 cls_qb[NCLS + 1];
 };
 
 template <int K>
@@ -262,19 +273,18 @@ __device__ __forceinline__ void layout_bases(u32 L, int ew, u64 (&T)[K], u64 (&F
   R = (u64)ew + 71ull * L * K;
 }
 
+// VARLEN: `job` is the queue entry (string | jq << 32) resolved at claim time
 template <bool VARLEN, int K, int M>
 __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u32& jq) {
   u64 s;
   if (VARLEN) {
-    const u64 e = P.job_map[job];
-    s = e & 0xffffffffull;
+    s = job & 0xffffffffull;
     const u64 o0 = P.offsets[s], o1 = P.offsets[s + 1];
     st.p = P.data + o0;
-    st.n = min(o1 - o0, P.n_bytes);  // clamp to the host-checked bound (plan_count_kernel)
-    const u64* mt = P.meta + 3 * s;
-    jq = (u32)(e >> 32);
-    st.scratch = mt[1];
-    st.cnt = mt[2];
+    st.n = min(o1 - o0, P.n_bytes);  // clamp to the host-checked bound (plan_queue_kernel)
+    jq = (u32)(job >> 32);
+    st.scratch = P.meta[2 * s];
+    st.cnt = P.meta[2 * s + 1];
   } else {
     // jq-major order: all strings' first jobs, then all second jobs, ...
     // Jobs of one jq have equal size, so static round-robin stays balanced.

@@ -3,14 +3,16 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
-#include <cub/device/device_scan.cuh>
 
 #include "../../include/halftime_b200.h"
 #include "hash_kernel.cuh"
+#include "small_kernel.cuh"
 #include "tail_kernel.cuh"
 #include "merge_kernel.cuh"
 
@@ -140,75 +142,61 @@ __global__ void fill_kernel(u64 seed, u64 woff, u64 n_words, u64 n_bytes, u64* d
   }
 }
 
-struct Tri {
-  u64 a, b, c;
+// Varlen plan (one kernel): per string its instance count; strings shorter
+// than one instance go to the tail list (tail_varlen_kernel), every other
+// string's jobs are appended to the queue of their size class (min(instances,
+// 64)); the hash kernel claims classes largest first (LPT scheduling with
+// dynamic claiming).  Queue order inside a class and the scratch/counter
+// bases of multi-job strings come from atomics: digests are integer sums and
+// do not depend on them.  err bit 1: a string longer than max_n; bit 2: more
+// instances than the declared total (queues would overflow; job dropped).
+struct QueueTable {
+  u64 qb[NCLS + 1];  // queue c occupies job_map[qb[c], qb[c+1])
 };
-struct TriSum {
-  __host__ __device__ Tri operator()(const Tri& x, const Tri& y) const { return {x.a + y.a, x.b + y.b, x.c + y.c}; }
-};
-
-// Varlen plan, pass 1: per string its job count, scratch and counter needs,
-// plus a histogram of job sizes (instances, capped at 64) for LPT ordering.
-constexpr int NCLS = 65;
 template <int OUT>
-__global__ void plan_count_kernel(const u64* off, u64 n, u64 max_n, int job_lvl, Tri* tri, int* err, u32* hist,
-                                  u32* tail_list, u32* tail_count) {
+__global__ void __launch_bounds__(256) plan_queue_kernel(const u64* off, u64 n, u64 max_n, int job_lvl,
+                                                         const __grid_constant__ QueueTable Q, int* err, u32* cls_cnt,
+                                                         u64* queues, u64* meta, unsigned long long* totals,
+                                                         u32* tail_list, u32* tail_count) {
   constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m;
-  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s <= n; s += (u64)gridDim.x * blockDim.x) {
-    if (s == n) {
-      tri[n] = {0, 0, 0};
-      continue;
+  const int lane = threadIdx.x & 31;
+  const u64 per = 1ull << (3 * job_lvl);
+  const u64 step = (u64)gridDim.x * blockDim.x;
+  // whole warps iterate together so the tail-list append can be aggregated
+  for (u64 s0 = (u64)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); s0 < n; s0 += step) {
+    const u64 s = s0 + lane;
+    u64 ni = 0;
+    bool tail = false;
+    if (s < n) {
+      u64 nb = off[s + 1] - off[s];
+      if (nb > max_n) {
+        atomicOr(err, 1);
+        nb = max_n;
+      }
+      ni = ((nb + 7) >> 3) / M;
+      tail = ni == 0;
     }
-    u64 nb = off[s + 1] - off[s];
-    if (nb > max_n) {
-      atomicOr(err, 1);
-      nb = max_n;
-    }
-    const u64 ni = ((nb + 7) >> 3) / M;
-    if (ni == 0) {  // shorter than one instance: tail_varlen_kernel, no job
-      tail_list[atomicAdd(tail_count, 1u)] = (u32)s;
-      tri[s] = {0, 0, 0};
-      continue;
-    }
+    const unsigned tm = __ballot_sync(0xffffffffu, tail);
+    u32 tb = 0;
+    if (lane == 0 && tm) tb = atomicAdd(tail_count, (u32)__popc(tm));
+    tb = __shfl_sync(0xffffffffu, tb, 0);
+    if (tail) tail_list[tb + __popc(tm & ((1u << lane) - 1))] = (u32)s;
+    if (s >= n || tail) continue;
     const u64 J = job_count(ni, job_lvl);
     u64 w, c;
     scratch_need(ni, K, job_lvl, &w, &c);
-    tri[s] = {J, w, c};
-    const u64 per = 1ull << (3 * job_lvl);
+    meta[2 * s] = w ? atomicAdd(totals, (unsigned long long)w) : 0;
+    meta[2 * s + 1] = c ? atomicAdd(totals + 1, (unsigned long long)c) : 0;
     for (u64 q = 0; q < J; q++) {
-      const u64 jn = ni > q * per ? min(per, ni - q * per) : 0;
-      atomicAdd(hist + (jn > 64 ? 64 : jn), 1u);
-    }
-  }
-}
-
-// Varlen plan, pass 2: scatter (string, job) pairs into the job map largest
-// job first (counting sort on the size class; order inside a class is
-// arbitrary -- digests do not depend on it).  With dynamic claiming this is
-// longest-processing-time-first scheduling.
-template <int OUT>
-__global__ void plan_scatter_kernel(const u64* off, u64 n, u64 max_n, int job_lvl, const u32* hist, u32* cursor,
-                                    u64* job_map) {
-  constexpr int M = Geo<Var<OUT>>::m;
-  __shared__ u32 base[NCLS];
-  if (threadIdx.x == 0) {
-    u32 acc = 0;
-    for (int c = NCLS - 1; c >= 0; c--) {
-      base[c] = acc;
-      acc += hist[c];
-    }
-  }
-  __syncthreads();
-  for (u64 s = blockIdx.x * (u64)blockDim.x + threadIdx.x; s < n; s += (u64)gridDim.x * blockDim.x) {
-    const u64 nb = min(off[s + 1] - off[s], max_n);
-    const u64 ni = ((nb + 7) >> 3) / M;
-    if (ni == 0) continue;  // handled by tail_varlen_kernel
-    const u64 J = job_count(ni, job_lvl), per = 1ull << (3 * job_lvl);
-    for (u64 q = 0; q < J; q++) {
-      const u64 jn = ni > q * per ? min(per, ni - q * per) : 0;
-      const int c = jn > 64 ? 64 : (int)jn;
-      const u32 pos = base[c] + atomicAdd(cursor + c, 1u);
-      job_map[pos] = s | (q << 32);
+      const u64 jn = min(per, ni - q * per);
+      const int cl = jn > 64 ? 64 : (int)jn;
+      const u32 pos = atomicAdd(cls_cnt + cl, 1u);
+      if (pos < Q.qb[cl + 1] - Q.qb[cl]) {
+        queues[Q.qb[cl] + pos] = s | (q << 32);
+      } else {
+        atomicSub(cls_cnt + cl, 1u);
+        atomicOr(err, 2);
+      }
     }
   }
 }
@@ -230,7 +218,7 @@ template <> struct KCfg<32> { static constexpr int W = 2, NS = 2, MINB = HTH_V24
 #define HTH_V40_NS 2
 #endif
 #ifndef HTH_V40_MINB
-#define HTH_V40_MINB 6
+#define HTH_V40_MINB 5
 #endif
 template <> struct KCfg<40> { static constexpr int W = HTH_V40_W, NS = HTH_V40_NS, MINB = HTH_V40_MINB; };
 
@@ -241,7 +229,8 @@ constexpr size_t smem_bytes() {
   // ring + mbarriers + parked level-1 group and level-3 accumulator +
   // claimed-job queue (+ per-job EHC seeds in many-seeds mode), per warp
   return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 9 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8 +
-                         (PS ? 2 * MAX_EW * 4 : 0));
+                         (PS ? 2 * MAX_EW * 4 : 0)) +
+         (NCLS + 1) * 4 + NCLS * 8;  // + varlen class table (per CTA)
 }
 
 int sm_count(int dev) {
@@ -253,22 +242,42 @@ int sm_count(int dev) {
   return cache[dev];
 }
 
+// Resident CTAs per SM of `kern` at (tpb, smem) on the current device; the
+// dynamic shared-memory limit is raised once per (kernel, device, smem) and
+// the answer cached, keeping the per-call host path to the launch itself.
+int occupancy(const void* kern, int tpb, size_t smem, int* dev_out, int* occ_out) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> limit;  // the attribute is per kernel: only raise it
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  *dev_out = dev;
+  const auto key = std::make_tuple(kern, dev, smem, tpb);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *occ_out = it->second;
+    return HTH_OK;
+  }
+  size_t& lim = limit[std::make_pair(kern, dev)];
+  if (smem > lim) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    lim = smem;
+  }
+  int o = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, tpb, smem));
+  cache[key] = *occ_out = std::max(o, 1);
+  return HTH_OK;
+}
+
 template <int OUT, bool VARLEN, bool AL8, bool PS = false>
 int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   constexpr int W = KCfg<OUT>::W, NS = KCfg<OUT>::NS;
   auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB, AL8, PS>;
   const size_t smem = smem_bytes<OUT, PS>();
-  static std::once_flag once[64];
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  static int occ[64] = {0};
-  std::call_once(once[dev & 63], [&]() {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, W * 32, smem);
-    occ[dev & 63] = o > 0 ? o : 1;
-  });
-  u64 grid = (u64)sm_count(dev) * occ[dev & 63];
+  int dev = 0, occ = 1;
+  if (int rc = occupancy((const void*)kern, W * 32, smem, &dev, &occ)) return rc;
+  u64 grid = (u64)sm_count(dev) * occ;
   const u64 need = ceil_div(n_jobs_bound, W);
   if (need < grid) grid = need;
   if (grid == 0) grid = 1;
@@ -277,25 +286,38 @@ int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   return HTH_OK;
 }
 
-template <int OUT, int CPT, bool MASKED>
-int launch_tail(const TailParams& P, cudaStream_t st) {
-  constexpr int NS = 4, TPB = 256;
-  auto kern = tail_kernel<OUT, CPT, MASKED, NS>;
-  const u64 sby = (2 * P.stride + 127) & ~127ull;
+#ifndef HTH_TAIL_NS
+#define HTH_TAIL_NS 1
+#endif
+#ifndef HTH_TAIL_STAGE
+#define HTH_TAIL_STAGE 8192
+#endif
+// NS stages of GP string pairs per warp; measured on config 3 (1 KiB strings):
+// one 8 KiB stage per warp streams best (6.33 TB/s vs 6.21 for 2 x 4 KiB and
+// 5.5 for 4 x 2 KiB), more than 64 KiB per 8-warp CTA costs occupancy
+template <int OUT, int CPT, bool MASKED, int GP>
+int launch_tail_g(const TailParams& P, cudaStream_t st) {
+  constexpr int NS = HTH_TAIL_NS, TPB = 256;
+  auto kern = tail_kernel<OUT, CPT, MASKED, NS, GP>;
+  const u64 sby = (GP * 2 * P.stride + 127) & ~127ull;
   const size_t smem = (TPB / 32) * NS * (sby + 8);
   if (smem > 227 * 1024) return fail(HTH_EINVAL, "tail kernel stage too large");
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TPB, smem));
-  const u64 pairs = (P.n_strings + 1) / 2;
+  int dev = 0, occ = 1;
+  if (int rc = occupancy((const void*)kern, TPB, smem, &dev, &occ)) return rc;
+  const u64 groups = ceil_div((P.n_strings + 1) / 2, (u64)GP);
   u64 grid = (u64)sm_count(dev) * std::max(occ, 1);
-  const u64 need = ceil_div(pairs, TPB / 32);
+  const u64 need = ceil_div(groups, TPB / 32);
   if (need < grid) grid = need;
   kern<<<(unsigned)std::max<u64>(grid, 1), TPB, smem, st>>>(P);
   CK(cudaGetLastError());
   return HTH_OK;
+}
+template <int OUT, int CPT, bool MASKED>
+int launch_tail(const TailParams& P, cudaStream_t st) {
+  const u64 pair = 2 * P.stride;
+  if (4 * pair <= HTH_TAIL_STAGE) return launch_tail_g<OUT, CPT, MASKED, 4>(P, st);
+  if (2 * pair <= HTH_TAIL_STAGE) return launch_tail_g<OUT, CPT, MASKED, 2>(P, st);
+  return launch_tail_g<OUT, CPT, MASKED, 1>(P, st);
 }
 
 template <int OUT, bool MASKED>
@@ -310,6 +332,45 @@ template <int OUT>
 int dispatch_tail(const TailParams& P, u64 nch, cudaStream_t st) {
   const bool masked = (P.n_bytes % 16) != 0 || (nch % 16) != 0;
   return masked ? dispatch_tail_m<OUT, true>(P, nch, st) : dispatch_tail_m<OUT, false>(P, nch, st);
+}
+
+#ifndef HTH_SMALL_STAGE
+#define HTH_SMALL_STAGE 8704
+#endif
+template <int OUT, int G>
+int launch_small(const Params& P, cudaStream_t st) {
+  constexpr int W = KCfg<OUT>::W, NS = 2;
+  auto kern = small_kernel<OUT, G, W, NS, KCfg<OUT>::MINB>;
+  const u64 sby = (G * P.stride + 16 + 127) & ~127ull;
+  const size_t smem = W * NS * (sby + 8);
+  int dev = 0, occ = 1;
+  if (int rc = occupancy((const void*)kern, W * 32, smem, &dev, &occ)) return rc;
+  u64 grid = (u64)sm_count(dev) * std::max(occ, 1);
+  const u64 need = ceil_div(ceil_div(P.n_strings, (u64)G), (u64)W);
+  if (need < grid) grid = need;
+  kern<<<(unsigned)std::max<u64>(grid, 1), W * 32, smem, st>>>(P);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+// strings per warp stage: about HTH_SMALL_STAGE bytes per contiguous copy,
+// fewer when the batch would not give every resident warp two stages
+template <int OUT>
+int dispatch_small(const Params& P, cudaStream_t st) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const u64 slots = 2ull * sm_count(dev) * KCfg<OUT>::W * KCfg<OUT>::MINB;
+  int g = 4 * P.stride <= HTH_SMALL_STAGE ? 4 : (2 * P.stride <= HTH_SMALL_STAGE ? 2 : 1);
+  while (g > 1 && ceil_div(P.n_strings, (u64)g) < slots) g >>= 1;
+  if (g == 4) return launch_small<OUT, 4>(P, st);
+  if (g == 2) return launch_small<OUT, 2>(P, st);
+  return launch_small<OUT, 1>(P, st);
+}
+// small_kernel applies: one level (1..7 instances), aligned strings packed
+// closely, and the partial final word (if any) in the tail, not in an instance
+bool small_ok(const VarInfo& v, u64 n_inst, u64 stride, u64 n_bytes, const void* data) {
+  const u64 nw = (n_bytes + 7) / 8;
+  return n_inst >= 1 && n_inst <= 7 && stride % 8 == 0 && (reinterpret_cast<uintptr_t>(data) & 7) == 0 &&
+         stride <= n_bytes + 256 && ((n_bytes & 7) == 0 || nw > n_inst * (u64)v.m);
 }
 
 template <bool VARLEN, bool AL8>
@@ -376,35 +437,37 @@ FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
 
 // varlen workspace geometry
 struct VarPlan {
-  u64 off_err, off_tri, off_meta, off_jobs, off_scr, off_cnt, off_acc, off_ev, off_ctl, off_hist, off_tail, off_cub,
-      cub_bytes, total,
-      max_jobs,
-      scr_words, cnts;
+  u64 off_err, off_cnt, off_acc, off_ev, off_ctl, off_pctl, off_clear, off_tail, off_meta, off_queue, off_scr, total,
+      max_jobs, q_inst, scr_words, cnts;
+  QueueTable Q;
 };
+// Workspace: the error flag (offset 0, hth_varlen_status), the self-resetting
+// hash state and the plan counters first (cleared by one memset per call),
+// then the tail list, per-string bases, class queues and merge scratch.
 int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
   const u64 total_inst = total_bytes / (8ull * v.m);
   p->max_jobs = n + total_inst / 64 + 1;
+  p->q_inst = total_inst;
   p->scr_words = (total_inst / 56 + 1) * 8ull * v.k;
   p->cnts = total_inst / 448 + 1;
-  size_t cub_bytes = 0;
-  cudaError_t e = cub::DeviceScan::ExclusiveScan(nullptr, cub_bytes, (Tri*)nullptr, (Tri*)nullptr, TriSum(),
-                                                 Tri{0, 0, 0}, (int64_t)(n + 1), (cudaStream_t)0);
-  if (e != cudaSuccess) return cuda_fail(e, "cub scan sizing");
-  p->cub_bytes = cub_bytes;
+  u64 qcap = 0;
+  for (int c = 0; c < NCLS; c++) {
+    p->Q.qb[c] = qcap;
+    qcap += queue_cap(c, p->max_jobs, p->q_inst);
+  }
+  p->Q.qb[NCLS] = qcap;
   u64 o = 0;
   p->off_err = o; o += 256;
-  p->off_tri = o; o = align_up(o + (n + 1) * sizeof(Tri), 256);
-  p->off_meta = o; o = align_up(o + (n + 1) * sizeof(Tri), 256);
-  p->off_jobs = o; o = align_up(o + p->max_jobs * 8, 256);
-  p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
-  // self-resetting state, contiguous so one memset per call clears it
   p->off_cnt = o; o = align_up(o + p->cnts * 4, 256);
   p->off_acc = o; o = align_up(o + n * v.k * 8, 256);
   p->off_ev = o; o = align_up(o + n * 4, 256);
   p->off_ctl = o; o += 256;
-  p->off_hist = o; o = align_up(o + 2 * NCLS * 4 + 4, 256);  // histogram + scatter cursors + tail count
+  p->off_pctl = o; o += 512;  // class counts [NCLS] u32 @0, tail count @320, scratch/counter totals @384
+  p->off_clear = o;
   p->off_tail = o; o = align_up(o + n * 4, 256);
-  p->off_cub = o; o = align_up(o + cub_bytes, 256);
+  p->off_meta = o; o = align_up(o + n * 16, 256);
+  p->off_queue = o; o = align_up(o + qcap * 8, 256);
+  p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
   p->total = o;
   return HTH_OK;
 }
@@ -591,6 +654,15 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
       case 40: return dispatch_tail<40>(T, nch, st);
     }
   }
+  if (small_ok(v, f.n_inst, n_strings > 1 ? stride_bytes : align_up(n_bytes, 8), n_bytes, d_data)) {
+    if (n_strings == 1) P.stride = align_up(n_bytes, 8);
+    switch (output_bytes) {
+      case 16: return dispatch_small<16>(P, st);
+      case 24: return dispatch_small<24>(P, st);
+      case 32: return dispatch_small<32>(P, st);
+      case 40: return dispatch_small<40>(P, st);
+    }
+  }
   uint8_t* ws = (uint8_t*)d_workspace;
   P.scratch = (u64*)ws;
   P.acc = (u64*)(ws + f.ws_scratch);
@@ -662,50 +734,25 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* ws = (uint8_t*)d_workspace;
   int* err = (int*)(ws + p.off_err);
-  Tri* tri = (Tri*)(ws + p.off_tri);
-  Tri* meta = (Tri*)(ws + p.off_meta);
-  u64* jobs = (u64*)(ws + p.off_jobs);
-  u32* hist = (u32*)(ws + p.off_hist);
-  u32* tail_count = hist + 2 * NCLS;
+  u32* cls_cnt = (u32*)(ws + p.off_pctl);
+  u32* tail_count = (u32*)(ws + p.off_pctl + 320);
+  auto* totals = (unsigned long long*)(ws + p.off_pctl + 384);
   u32* tail_list = (u32*)(ws + p.off_tail);
-  CK(cudaMemsetAsync(err, 0, 4, st));
+  u64* meta = (u64*)(ws + p.off_meta);
+  u64* queues = (u64*)(ws + p.off_queue);
   // plan areas of an earlier call may overlap this call's counters/accumulators
-  CK(cudaMemsetAsync(ws + p.off_cnt, 0, p.off_cub - p.off_cnt, st));
-  const u64 blocks = std::min<u64>(ceil_div(n_strings + 1, 256), 4096);
+  CK(cudaMemsetAsync(ws, 0, p.off_clear, st));
   const int job_lvl = pick_job_lvl(((max_n_bytes + 7) / 8) / (u64)v.m);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const unsigned pb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 256), (u64)sm_count(dev) * 8));
   switch (output_bytes) {
-    case 16: plan_count_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
-    case 24: plan_count_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
-    case 32: plan_count_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
-    case 40: plan_count_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, tri, err, hist, tail_list, tail_count); break;
+    case 16: plan_queue_kernel<16><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
+    case 24: plan_queue_kernel<24><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
+    case 32: plan_queue_kernel<32><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
+    case 40: plan_queue_kernel<40><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
   }
   CK(cudaGetLastError());
-  size_t cub_bytes = p.cub_bytes;
-  CK(cub::DeviceScan::ExclusiveScan(ws + p.off_cub, cub_bytes, tri, meta, TriSum(), Tri{0, 0, 0},
-                                    (int64_t)(n_strings + 1), st));
-  switch (output_bytes) {
-    case 16: plan_scatter_kernel<16><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
-    case 24: plan_scatter_kernel<24><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
-    case 32: plan_scatter_kernel<32><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
-    case 40: plan_scatter_kernel<40><<<(unsigned)blocks, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, hist, hist + NCLS, jobs); break;
-  }
-  CK(cudaGetLastError());
-  Params P{};
-  P.data = (const uint8_t*)d_data;
-  P.n_strings = n_strings;
-  P.offsets = d_offsets;
-  P.job_map = jobs;
-  P.meta = (const u64*)meta;
-  P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_count)
-  P.S = d_seed;
-  P.out = d_out;
-  P.job_lvl = job_lvl;
-  fill_ehc(v, seed_fold, P);
-  P.scratch = (u64*)(ws + p.off_scr);
-  P.counters = (u32*)(ws + p.off_cnt);
-  P.acc = (u64*)(ws + p.off_acc);
-  P.events = (u32*)(ws + p.off_ev);
-  set_ctl(P, ws + p.off_ctl);
   {
     TailVarParams T{};
     T.data = (const uint8_t*)d_data;
@@ -718,8 +765,6 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
     T.F0 = (u64)v.ew + 7ull * v.k;
     T.Fstep = 64;
     T.out = d_out;
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
     const unsigned tb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 16), (u64)sm_count(dev) * 8));
     switch (output_bytes) {
       case 16: tail_varlen_kernel<16><<<tb, 256, 0, st>>>(T); break;
@@ -729,6 +774,25 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
     }
     CK(cudaGetLastError());
   }
+  Params P{};
+  P.data = (const uint8_t*)d_data;
+  P.n_strings = n_strings;
+  P.offsets = d_offsets;
+  P.job_map = queues;
+  P.meta = meta;
+  P.cls_cnt = cls_cnt;
+  P.n_jobs = p.max_jobs;  // varlen: queue sizing bound; the kernel counts the jobs itself
+  memcpy(P.cls_qb, p.Q.qb, sizeof(P.cls_qb));
+  P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_queue_kernel)
+  P.S = d_seed;
+  P.out = d_out;
+  P.job_lvl = job_lvl;
+  fill_ehc(v, seed_fold, P);
+  P.scratch = (u64*)(ws + p.off_scr);
+  P.counters = (u32*)(ws + p.off_cnt);
+  P.acc = (u64*)(ws + p.off_acc);
+  P.events = (u32*)(ws + p.off_ev);
+  set_ctl(P, ws + p.off_ctl);
   return dispatch<true>(output_bytes, P, p.max_jobs, st);
 }
 
@@ -737,7 +801,8 @@ int hth_varlen_status(void* d_workspace, void* stream) {
   int h = 0;
   CK(cudaMemcpyAsync(&h, d_workspace, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
-  if (h) return fail(HTH_ESEEDSIZE, "a string was longer than max_n_bytes; its digest is invalid");
+  if (h & 1) return fail(HTH_ESEEDSIZE, "a string was longer than max_n_bytes; its digest is invalid");
+  if (h & 2) return fail(HTH_EINVAL, "the strings hold more bytes than total_bytes declared; digests are invalid");
   return HTH_OK;
 }
 

@@ -1,6 +1,7 @@
 // HalftimeHash B200 engine: the persistent warp-job hash kernel.
 // Decomposition and invariants: engine.cuh.  Reference citations inline.
 #pragma once
+#include <type_traits>
 #include "engine.cuh"
 
 #ifndef HTH_STATIC_FIRST
@@ -63,17 +64,17 @@ struct EhcSrc {
   __device__ __forceinline__ u32 hi(int i) const { return PERSEED ? sm[2 * i + 1] : P.ehc[2 * i + 1]; }
 };
 
-// EHC leaf of instances q and q+4 of the stage, lane j -> CA[r], CB[r]
-// (hasher.py:356-364; ehc.py:102-118).
+// EHC leaf of two instances, lane j -> CA[r], CB[r] (hasher.py:356-364;
+// ehc.py:102-118).  offA/offB: word offset of lane j's first word of each
+// instance in the stage (instance base * m + j).
 template <int OUT, bool AL, class EH>
-__device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int j, const EH& P,
-                                      u64 (&CA)[Var<OUT>::k], u64 (&CB)[Var<OUT>::k]) {
+__device__ __forceinline__ void leaf2o(const uint8_t* buf, u32 delta, u32 offA, u32 offB, const EH& P,
+                                       u64 (&CA)[Var<OUT>::k], u64 (&CB)[Var<OUT>::k]) {
   using V = Var<OUT>;
-  constexpr int K = V::k, E = V::e, D = V::d, WB = V::w, M = Geo<V>::m, NP = E - D;
+  constexpr int K = V::k, E = V::e, D = V::d, WB = V::w, NP = E - D;
   u64 HA[E], HB[E];
 #pragma unroll
   for (int i = 0; i < E; i++) HA[i] = HB[i] = 0;
-  const u32 offA = (u32)(q * M + j), offB = (u32)((q + 4) * M + j);
 #pragma unroll
   for (int u = 0; u < WB; u++) {
     w2 xa[D], xb[D];
@@ -140,6 +141,14 @@ __device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int 
     CA[r] = a;
     CB[r] = b;
   }
+}
+
+// instances q and q+4 of an 8-instance round
+template <int OUT, bool AL, class EH>
+__device__ __forceinline__ void leaf2(const uint8_t* buf, u32 delta, int q, int j, const EH& P,
+                                      u64 (&CA)[Var<OUT>::k], u64 (&CB)[Var<OUT>::k]) {
+  constexpr int M = Geo<Var<OUT>>::m;
+  leaf2o<OUT, AL>(buf, delta, (u32)(q * M + j), (u32)((q + 4) * M + j), P, CA, CB);
 }
 
 // Seed-region bases of a layout with L levels (hasher.py:130-153), computed
@@ -242,7 +251,6 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   }
   __syncwarp();
 
-  const u64 n_jobs = VARLEN ? P.meta[3 * P.n_strings] : P.n_jobs;
   const int job_lvl = P.job_lvl;
   SeedSrc<PS> sd{P.S, 0};
   const u64 pol = policy_evict_first();
@@ -257,6 +265,27 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // PS: this warp's EHC seed words for the current job, (lo, hi) pairs
   u32* ehc_sm = reinterpret_cast<u32*>(jq_buf + (W - warp) * QN) + warp * 2 * MAX_EW;
   const EhcSrc<PS> eh{P, ehc_sm};
+  // varlen: per size class its first job id (largest class first);
+  // cls_pre[0] = total jobs = end of class 1
+  u32* cls_pre = reinterpret_cast<u32*>(smem + W * NS * SB + W * NS * 8 + W * NACC * 8 + W * QN * 8 +
+                                        (PS ? W * 2 * MAX_EW * 4 : 0));
+  u64 n_jobs = P.n_jobs;
+  if (VARLEN) {
+    for (int c = threadIdx.x; c < NCLS; c += blockDim.x) cls_pre[c] = c ? P.cls_cnt[c] : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u32 acc = 0;
+      for (int c = NCLS - 1; c >= 1; c--) {
+        const u32 k = cls_pre[c];
+        cls_pre[c] = acc;
+        acc += k;
+      }
+      cls_pre[0] = acc;
+    }
+    __syncthreads();
+    n_jobs = cls_pre[0];
+  }
+  int ccur = NCLS - 1;  // varlen: class of this warp's latest claim (ids only grow)
   u32 qhead = 0, qtail = 0;        // queue: [qtail, qhead) claimed, not yet started
   bool pdone = false;
   // the first job of every warp is static (job = global warp index), so the
@@ -285,12 +314,17 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       pdone = true;
       return false;
     }
-    if (lane == 0) jq_buf[qhead % QN] = jc;
+    u64 e = jc;
+    if (VARLEN) {  // job id -> class queue entry
+      while (jc >= cls_pre[ccur - 1]) ccur--;
+      e = P.job_map[P.cls_qb[ccur] + (jc - cls_pre[ccur])];
+    }
+    if (lane == 0) jq_buf[qhead % QN] = e;
     qhead++;
     Str st;
     u32 jq, ni;
     u64 b0;
-    decode_job<VARLEN, K, M>(P, jc, st, jq);
+    decode_job<VARLEN, K, M>(P, e, st, jq);
     job_span<M>(st, jq, job_lvl, b0, prem, ni);
     psrc = reinterpret_cast<u64>(st.p) + b0;
     return true;
@@ -372,127 +406,138 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     const u64 len1 = st.n_inst >> 3, full1 = len1 & ~7ull;
     const u64 len2 = st.n_inst >> 6, full2 = len2 & ~7ull;
 
-    for (u32 c = 0; c < nchunks; c++) {
-      const u32 slot = cseq % NS;
-      mbar_wait(&bars[slot], (cseq / NS) & 1);
-      uint8_t* buf = ring + slot * SB;
-      const bool tail_chunk = last_job && (c + 1 == nchunks);
-      if (tail_chunk && (st.n & 7)) {
-        // zero-pad the partial final word (hasher.py:179-183, 416-419)
-        const u32 endpos = delta + (u32)(nbytes - (u64)c * CB);
-        const u32 nz = 8 - (u32)(st.n & 7);
-        if ((u32)lane < nz) buf[endpos + lane] = 0;
-        fence_proxy_async();
-        __syncwarp();
-      }
-      const u32 r0 = c * ROUND_INST;  // first instance of the round (job-relative)
-      if (r0 < ninst) {
-        u64 CA[K], CB_[K];
-        if (!AL8 && (delta & 7))
-          leaf2<OUT, false>(buf, delta, q, j, eh, CA, CB_);
-        else
-          leaf2<OUT, true>(buf, delta, q, j, eh, CA, CB_);
-        const u64 G1 = (inst0 >> 3) + c;  // level-1 group of this round
-        if (G1 < len1) {
-          // complete group -> level-1 node (nh_tree_node: last block added)
-          u64 B1[K];
-#pragma unroll
-          for (int r = 0; r < K; r++) {
-            // level-0 seeds S[T_r + q] (tree.py:55-60); L1-resident
-#if HTH_S1_REGS
-            u64 v = nh_acc(0, CA[r], s1A[r]);
-            v = (q < 3) ? nh_acc(v, CB_[r], s1B[r]) : v + CB_[r];
-#else
-            u64 v = nh_acc(0, CA[r], sd(tc.T(r) + q));
-            v = (q < 3) ? nh_acc(v, CB_[r], sd(tc.T(r) + q + 4)) : v + CB_[r];
-#endif
-            v += shfl_xor(v, 8);
-            v += shfl_xor(v, 16);
-            B1[r] = v;
-          }
-          const int p1 = (int)(G1 & 7);
-          if (G1 >= full1) {
-            if (q == 0) {  // level-1 leftover -> finalize slot (1, p1)
-#pragma unroll
-              for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B1[r], sd(tc.F(r) + 56 + p1 * 8 + j));
+    // A full job (not the string's last, exactly 8^job_lvl instances) has no
+    // tail, no partial round and no leftover groups below its root: its
+    // round loop is instantiated without those checks (fixed batches; varlen
+    // keeps one body for a small instruction footprint).
+    auto rounds = [&](auto full_c) {
+      constexpr bool FULL = decltype(full_c)::value;
+      for (u32 c = 0; c < nchunks; c++) {
+        const u32 slot = cseq % NS;
+        mbar_wait(&bars[slot], (cseq / NS) & 1);
+        uint8_t* buf = ring + slot * SB;
+        const bool tail_chunk = !FULL && last_job && (c + 1 == nchunks);
+        if (tail_chunk && (st.n & 7)) {
+          // zero-pad the partial final word (hasher.py:179-183, 416-419)
+          const u32 endpos = delta + (u32)(nbytes - (u64)c * CB);
+          const u32 nz = 8 - (u32)(st.n & 7);
+          if ((u32)lane < nz) buf[endpos + lane] = 0;
+          fence_proxy_async();
+          __syncwarp();
+        }
+        const u32 r0 = c * ROUND_INST;  // first instance of the round (job-relative)
+        if (FULL || r0 < ninst) {
+          u64 CA[K], CB_[K];
+          if (VARLEN || (!AL8 && (delta & 7)))
+            leaf2<OUT, false>(buf, delta, q, j, eh, CA, CB_);
+          else
+            leaf2<OUT, true>(buf, delta, q, j, eh, CA, CB_);
+          const u64 G1 = (inst0 >> 3) + c;  // level-1 group of this round
+          if (FULL || G1 < len1) {
+            // complete group -> level-1 node (nh_tree_node: last block added)
+            u64 B1[K];
+  #pragma unroll
+            for (int r = 0; r < K; r++) {
+              // level-0 seeds S[T_r + q] (tree.py:55-60); L1-resident
+  #if HTH_S1_REGS
+              u64 v = nh_acc(0, CA[r], s1A[r]);
+              v = (q < 3) ? nh_acc(v, CB_[r], s1B[r]) : v + CB_[r];
+  #else
+              u64 v = nh_acc(0, CA[r], sd(tc.T(r) + q));
+              v = (q < 3) ? nh_acc(v, CB_[r], sd(tc.T(r) + q + 4)) : v + CB_[r];
+  #endif
+              v += shfl_xor(v, 8);
+              v += shfl_xor(v, 16);
+              B1[r] = v;
             }
-          } else {
-            // park the level-1 block (lanes 0-7); every 8th round all 32 lanes
-            // form the level-2 node from the parked group
-            if (q == 0) {
-#pragma unroll
-              for (int r = 0; r < K; r++) nacc[(p1 * K + r) * 8 + j] = B1[r];
-            }
-            if (p1 == 7) {
-              __syncwarp();
-              const u64 G2 = G1 >> 3;  // level-2 block complete (replicated in all lanes)
-              u64 B2[K];
-#pragma unroll
-              for (int r = 0; r < K; r++) {
-                const u64 a = nacc[(q * K + r) * 8 + j], b = nacc[((q + 4) * K + r) * 8 + j];
-                u64 v = nh_acc(0, a, sd(tc.T(r) + 7 + q));
-                v = (q < 3) ? nh_acc(v, b, sd(tc.T(r) + 11 + q)) : v + b;
-                v += shfl_xor(v, 8);
-                v += shfl_xor(v, 16);
-                B2[r] = v;
+            const int p1 = (int)(G1 & 7);
+            if (!FULL && G1 >= full1) {
+              if (q == 0) {  // level-1 leftover -> finalize slot (1, p1)
+  #pragma unroll
+                for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B1[r], sd(tc.F(r) + 56 + p1 * 8 + j));
               }
-              __syncwarp();
-              if (job_lvl == 2) {
-                events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, B2, fin, lane, sd);
-              } else {
-                const int p2 = (int)(G2 & 7);
-                if (lane < 8) {
-                  if (G2 >= full2) {
-#pragma unroll
-                    for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B2[r], sd(tc.F(r) + 112 + p2 * 8 + j));
-                  } else {
-#pragma unroll
-                    for (int r = 0; r < K; r++) {
-                      const u64 a = n3acc[r * 8 + j];
-                      n3acc[r * 8 + j] = (p2 < 7) ? nh_acc(a, B2[r], sd(tc.T(r) + 14 + p2)) : a + B2[r];
-                    }
-                  }
+            } else {
+              // park the level-1 block (lanes 0-7); every 8th round all 32 lanes
+              // form the level-2 node from the parked group
+              if (q == 0) {
+  #pragma unroll
+                for (int r = 0; r < K; r++) nacc[(p1 * K + r) * 8 + j] = B1[r];
+              }
+              if (p1 == 7) {
+                __syncwarp();
+                const u64 G2 = G1 >> 3;  // level-2 block complete (replicated in all lanes)
+                u64 B2[K];
+  #pragma unroll
+                for (int r = 0; r < K; r++) {
+                  const u64 a = nacc[(q * K + r) * 8 + j], b = nacc[((q + 4) * K + r) * 8 + j];
+                  u64 v = nh_acc(0, a, sd(tc.T(r) + 7 + q));
+                  v = (q < 3) ? nh_acc(v, b, sd(tc.T(r) + 11 + q)) : v + b;
+                  v += shfl_xor(v, 8);
+                  v += shfl_xor(v, 16);
+                  B2[r] = v;
                 }
                 __syncwarp();
-                if (G2 < full2 && p2 == 7) {
-                  u64 B3[K];
-#pragma unroll
-                  for (int r = 0; r < K; r++) {
-                    B3[r] = lane < 8 ? n3acc[r * 8 + j] : 0;
-                    if (lane < 8) n3acc[r * 8 + j] = 0;
+                if (job_lvl == 2) {
+                  events += climb<K, Geo<V>::ew>(P, st, tc, 2, G2, B2, fin, lane, sd);
+                } else {
+                  const int p2 = (int)(G2 & 7);
+                  if (lane < 8) {
+                    if (!FULL && G2 >= full2) {
+  #pragma unroll
+                      for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], B2[r], sd(tc.F(r) + 112 + p2 * 8 + j));
+                    } else {
+  #pragma unroll
+                      for (int r = 0; r < K; r++) {
+                        const u64 a = n3acc[r * 8 + j];
+                        n3acc[r * 8 + j] = (p2 < 7) ? nh_acc(a, B2[r], sd(tc.T(r) + 14 + p2)) : a + B2[r];
+                      }
+                    }
                   }
-                  events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, B3, fin, lane, sd);
+                  __syncwarp();
+                  if ((FULL || G2 < full2) && p2 == 7) {
+                    u64 B3[K];
+  #pragma unroll
+                    for (int r = 0; r < K; r++) {
+                      B3[r] = lane < 8 ? n3acc[r * 8 + j] : 0;
+                      if (lane < 8) n3acc[r * 8 + j] = 0;
+                    }
+                    events += climb<K, Geo<V>::ew>(P, st, tc, 3, G2 >> 3, B3, fin, lane, sd);
+                  }
                 }
               }
             }
-          }
-        } else {
-          // incomplete last group: level-0 leftovers -> finalize slot (0, pos)
-          const u64 gA = inst0 + r0 + q, gB = gA + 4;
-          const bool vA = r0 + q < ninst, vB = r0 + q + 4 < ninst;
-#pragma unroll
-          for (int r = 0; r < K; r++) {
-            if (vA) fin[r] = nh_acc(fin[r], CA[r], sd(tc.F(r) + (gA & 7) * 8 + j));
-            if (vB) fin[r] = nh_acc(fin[r], CB_[r], sd(tc.F(r) + (gB & 7) * 8 + j));
+          } else {
+            // incomplete last group: level-0 leftovers -> finalize slot (0, pos)
+            const u64 gA = inst0 + r0 + q, gB = gA + 4;
+            const bool vA = r0 + q < ninst, vB = r0 + q + 4 < ninst;
+  #pragma unroll
+            for (int r = 0; r < K; r++) {
+              if (vA) fin[r] = nh_acc(fin[r], CA[r], sd(tc.F(r) + (gA & 7) * 8 + j));
+              if (vB) fin[r] = nh_acc(fin[r], CB_[r], sd(tc.F(r) + (gB & 7) * 8 + j));
+            }
           }
         }
-      }
-      if (tail_chunk) {
-        // Toeplitz tail: Rem_r = sum_i NH(Y_i, S[R + r + i])  (hasher.py:407-412)
-        const u64 tw0 = st.n_inst * M;
-        const u64 nw = (st.n + 7) >> 3;
-        const u32 cw0 = (u32)(tw0 - (inst0 * M + (u64)c * ROUND_INST * M));
-        const u32 nt = (u32)(nw - tw0);
-        for (u32 t = lane; t < nt; t += 32) {
-          const u64 y = (!AL8 && (delta & 7)) ? ld_word<false>(buf, delta, cw0 + t) : ld_word<true>(buf, delta, cw0 + t);
-#pragma unroll
-          for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], y, sd(tc.R() + r + t));
+        if (tail_chunk) {
+          // Toeplitz tail: Rem_r = sum_i NH(Y_i, S[R + r + i])  (hasher.py:407-412)
+          const u64 tw0 = st.n_inst * M;
+          const u64 nw = (st.n + 7) >> 3;
+          const u32 cw0 = (u32)(tw0 - (inst0 * M + (u64)c * ROUND_INST * M));
+          const u32 nt = (u32)(nw - tw0);
+          for (u32 t = lane; t < nt; t += 32) {
+            const u64 y = (VARLEN || (!AL8 && (delta & 7))) ? ld_word<false>(buf, delta, cw0 + t) : ld_word<true>(buf, delta, cw0 + t);
+  #pragma unroll
+            for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], y, sd(tc.R() + r + t));
+          }
         }
+        __syncwarp();
+        cseq++;
+        p_issue();
       }
-      __syncwarp();
-      cseq++;
-      p_issue();
-    }
+    };
+    if (!VARLEN && !last_job && ninst == (1u << (3 * job_lvl)))
+      rounds(std::true_type{});
+    else
+      rounds(std::false_type{});
 
     if (last_job && P.fin_const_ok) {
       if (lane == 0) {

@@ -1,0 +1,125 @@
+// HalftimeHash B200 engine: packed kernel for fixed batches of short
+// multi-instance strings (1 <= n_inst <= 7, e.g. 2000-byte strings of the
+// 40-byte variant, config 1's 4 KiB strings of the 24-byte variant).
+//
+// Such a string has one level only: every instance is a level-0 leftover, so
+// (tree.py:103-134, hasher.py:387-412)
+//   D_r = sum_i NH(C_i[r], S[F_r + 8 i ..]) + zero slots + tag + Toeplitz tail
+// with no tree nodes at all.  The job kernel would spend a whole 8-instance
+// round on each such string (2 of 8 slots busy for 2-instance strings); here
+// a warp stage holds G consecutive strings (one contiguous cp.async.bulk
+// copy), the 4/G eight-lane groups of each string take its instance pairs in
+// turn (the same two-instance bit-plane leaf as the job kernel), the
+// string's 32/G lanes share its tail words, and a butterfly over those lanes
+// yields the digest.  The zero-slot and tag terms are the host-precomputed
+// launch constants (fill_fin_const).
+#pragma once
+#include "hash_kernel.cuh"
+
+namespace hth {
+
+template <int OUT, int G, int W, int NS, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB) small_kernel(const __grid_constant__ Params P) {
+  using V = Var<OUT>;
+  constexpr int K = V::k, M = Geo<V>::m;
+  constexpr int LPS = 32 / G;  // lanes per string
+  constexpr int QG = 4 / G;    // eight-lane groups per string
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gs = lane / LPS, h = lane % LPS, qi = h >> 3, j = lane & 7;
+
+  const u64 n = P.n_bytes, stride = P.stride;
+  const u32 SBY = (u32)((G * stride + 16 + 127) & ~127ull);
+  uint8_t* ring = smem + (size_t)warp * NS * SBY;
+  u64* bars = reinterpret_cast<u64*>(smem + (size_t)W * NS * SBY) + warp * NS;
+  if (lane == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    fence_proxy_async();
+  }
+  __syncwarp();
+
+  const u64 nw = (n + 7) >> 3;
+  const u32 n_inst = (u32)(nw / M);
+  const u32 npairs = (n_inst + 1) >> 1;
+  const u32 nit = (npairs + QG - 1) / QG;  // leaf steps per string (launch-uniform)
+  const u32 tw0 = n_inst * M, nt = (u32)(nw - tw0);
+  const u64 last_mask = (n & 7) ? (1ull << (8 * (n & 7))) - 1 : ~0ull;
+  TreeCtx<K, Geo<V>::ew> tc;
+  tc.L = 1;  // n_inst < 8: a single level (hasher.py:130-153)
+  const SeedSrc<false> sd{P.S, 0};
+  const EhcSrc<false> eh{P, nullptr};
+  const u64 units = (P.n_strings + G - 1) / G;
+  const u64 NW = (u64)gridDim.x * W;
+  const u64 w0 = (u64)blockIdx.x * W + warp;
+  const u64 pol = policy_evict_first();
+
+  u64 pnext = w0;
+  u32 pseq = 0;
+  auto issue = [&]() {
+    if (pnext >= units) return;
+    const u64 s0 = pnext * G;
+    const u64 cnt = min((u64)G, P.n_strings - s0);
+    const u64 src = reinterpret_cast<u64>(P.data) + s0 * stride;
+    const u64 a0 = src & ~15ull;
+    const u32 bytes = (u32)(((src + (cnt - 1) * stride + n + 15) & ~15ull) - a0);
+    const u32 slot = pseq % NS;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[slot], bytes);
+      bulk_g2s(ring + slot * SBY, reinterpret_cast<const void*>(a0), bytes, &bars[slot], pol);
+    }
+    pseq++;
+    pnext += NW;
+  };
+#pragma unroll
+  for (int s = 0; s < NS; s++) issue();
+
+  u32 cseq = 0;
+  for (u64 u = w0; u < units; u += NW) {
+    const u32 slot = cseq % NS;
+    mbar_wait(&bars[slot], (cseq / NS) & 1);
+    const u64 s = u * G + gs;
+    const bool live = s < P.n_strings;
+    // this string's first byte in the stage (8-byte aligned: AL8 batches only)
+    const u32 delta = (u32)((reinterpret_cast<u64>(P.data) + u * G * stride) & 15) + (u32)(gs * stride);
+    const uint8_t* buf = ring + slot * SBY;
+    u64 fin[K];
+#pragma unroll
+    for (int r = 0; r < K; r++) fin[r] = 0;
+#pragma unroll 1
+    for (u32 it = 0; it < nit; it++) {
+      const u32 iA = 2 * (it * QG + qi), iB = iA + 1;
+      const bool vA = iA < n_inst, vB = iB < n_inst;
+      u64 CA[K], CB_[K];
+      leaf2o<OUT, true>(buf, delta, (vA ? iA : 0) * M + j, (vB ? iB : 0) * M + j, eh, CA, CB_);
+      // level-0 leftovers -> finalize slots iA, iB (tree.py:103-134)
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        if (vA) fin[r] = nh_acc(fin[r], CA[r], sd(tc.F(r) + iA * 8 + j));
+        if (vB) fin[r] = nh_acc(fin[r], CB_[r], sd(tc.F(r) + iB * 8 + j));
+      }
+    }
+    // Toeplitz tail: Rem_r = sum_t NH(Y_t, S[R + r + t])  (hasher.py:407-412)
+    for (u32 t = h; t < nt; t += LPS) {
+      u64 y = ld_word<true>(buf, delta, tw0 + t);
+      if (t + 1 == nt) y &= last_mask;  // zero-pad the partial final word (hasher.py:179-183)
+#pragma unroll
+      for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], y, sd(tc.R() + r + t));
+    }
+    __syncwarp();
+    cseq++;
+    issue();  // refill the slot just read
+#pragma unroll
+    for (int m = 1; m < LPS; m <<= 1) {
+#pragma unroll
+      for (int r = 0; r < K; r++) fin[r] += shfl_xor(fin[r], m);
+    }
+    u64 mine = 0;
+#pragma unroll
+    for (int r = 0; r < K; r++)
+      if (h == r) mine = fin[r] + P.fin_const[r];
+    if (live && h < K) P.out[s * K + h] = mine;
+  }
+}
+
+}  // namespace hth

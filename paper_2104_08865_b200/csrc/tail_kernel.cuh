@@ -71,10 +71,11 @@ __device__ __forceinline__ int scatter_index(int g) {
   return idx;
 }
 
-// Per warp: a ring of NS stages, each one cp.async.bulk copy of a PAIR of
-// consecutive strings (2 x stride bytes), so the loads stay deep in flight
-// without holding registers.  MASKED: n % 16 != 0 (partial words / chunks).
-template <int OUT, int CPT, bool MASKED, int NS>
+// Per warp: a ring of NS stages, each one cp.async.bulk copy of GP PAIRS of
+// consecutive strings (2 GP x stride bytes), so the loads stay deep in flight
+// without holding registers and each copy is large enough to stream at full
+// HBM rate.  MASKED: n % 16 != 0 (partial words / chunks).
+template <int OUT, int CPT, bool MASKED, int NS, int GP>
 __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ TailParams P) {
   constexpr int K = Var<OUT>::k;
   constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
@@ -83,8 +84,8 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
   const u64 n = P.n_bytes;
   const u32 nw = (u32)((n + 7) >> 3);
   const u32 nch = (u32)((n + 15) >> 4);
-  const u32 stage_bytes = (u32)(2 * P.stride);
-  const u32 SBY = (stage_bytes + 127) & ~127u;
+  const u32 pair_bytes = (u32)(2 * P.stride);
+  const u32 SBY = (GP * pair_bytes + 127) & ~127u;
   uint8_t* ring = smem + (size_t)warp * NS * SBY;
   u64* bars = reinterpret_cast<u64*>(smem + (size_t)(blockDim.x >> 5) * NS * SBY) + warp * NS;
   if (lane == 0) {
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
   const u64 NW = (u64)gridDim.x * (blockDim.x >> 5);
   const u64 w0 = (u64)blockIdx.x * (blockDim.x >> 5) + warp;
   const u64 pairs = (P.n_strings + 1) >> 1;
+  const u64 groups = (pairs + GP - 1) / GP;
   const int myidx = scatter_index<K>(g);
   const u64 pol = policy_evict_first();
   const u64 total_bytes = (P.n_strings - 1) * P.stride + ((n + 15) & ~15ull);
@@ -120,9 +122,9 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
   u64 pnext = w0;
   u32 pseq = 0;
   auto issue = [&]() {
-    if (pnext >= pairs) return;
-    const u64 off = 2 * pnext * P.stride;
-    const u32 bytes = (u32)min((u64)stage_bytes, total_bytes - off);
+    if (pnext >= groups) return;
+    const u64 off = (u64)GP * pnext * pair_bytes;
+    const u32 bytes = (u32)min((u64)GP * pair_bytes, total_bytes - off);
     const u32 slot = pseq % NS;
     if (lane == 0) {
       mbar_arrive_expect_tx(&bars[slot], bytes);
@@ -135,42 +137,49 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
   for (int s = 0; s < NS; s++) issue();
 
   u32 cseq = 0;
-  for (u64 pr = w0; pr < pairs; pr += NW) {
+  for (u64 gi = w0; gi < groups; gi += NW) {
     const u32 slot = cseq % NS;
     mbar_wait(&bars[slot], (cseq / NS) & 1);
-    const uint8_t* sb = ring + slot * SBY + (u32)half * (u32)P.stride;
-    uint4 v[CPT];
+#pragma unroll 1
+    for (int gp = 0; gp < GP; gp++) {
+      const u64 pr = gi * GP + gp;
+      if (GP > 1 && pr >= pairs) break;
+      const uint8_t* sb = ring + slot * SBY + (u32)gp * pair_bytes + (u32)half * (u32)P.stride;
+      uint4 v[CPT];
 #pragma unroll
-    for (int i = 0; i < CPT; i++) {
-      const u32 c = (u32)g + 16u * i;
-      v[i] = (!MASKED || c < nch) ? *reinterpret_cast<const uint4*>(sb + 16u * c) : make_uint4(0, 0, 0, 0);
-    }
-    __syncwarp();
-    cseq++;
-    issue();  // refill the slot just read
-    u64 acc[K];
+      for (int i = 0; i < CPT; i++) {
+        const u32 c = (u32)g + 16u * i;
+        v[i] = (!MASKED || c < nch) ? *reinterpret_cast<const uint4*>(sb + 16u * c) : make_uint4(0, 0, 0, 0);
+      }
+      if (gp == GP - 1) {
+        __syncwarp();
+        issue();  // refill the slot just read
+      }
+      u64 acc[K];
 #pragma unroll
-    for (int r = 0; r < K; r++) acc[r] = 0;
+      for (int r = 0; r < K; r++) acc[r] = 0;
 #pragma unroll
-    for (int i = 0; i < CPT; i++) {
-      const u32 c = (u32)g + 16u * i;
-      if (!MASKED || c < nch) {
-        w2 x0 = {v[i].x, v[i].y}, x1 = {v[i].z, v[i].w};
-        if (MASKED) {
-          x0 = mk((((u64)v[i].y << 32) | v[i].x) & mask0[i]);
-          x1 = mk((((u64)v[i].w << 32) | v[i].z) & mask1[i]);
-        }
-        const bool w1 = !MASKED || 2 * c + 1 < nw;
+      for (int i = 0; i < CPT; i++) {
+        const u32 c = (u32)g + 16u * i;
+        if (!MASKED || c < nch) {
+          w2 x0 = {v[i].x, v[i].y}, x1 = {v[i].z, v[i].w};
+          if (MASKED) {
+            x0 = mk((((u64)v[i].y << 32) | v[i].x) & mask0[i]);
+            x1 = mk((((u64)v[i].w << 32) | v[i].z) & mask1[i]);
+          }
+          const bool w1 = !MASKED || 2 * c + 1 < nw;
 #pragma unroll
-        for (int r = 0; r < K; r++) {
-          acc[r] = nh_acc(acc[r], x0, klo[i][r], khi[i][r]);
-          if (w1) acc[r] = nh_acc(acc[r], x1, klo[i][r + 1], khi[i][r + 1]);
+          for (int r = 0; r < K; r++) {
+            acc[r] = nh_acc(acc[r], x0, klo[i][r], khi[i][r]);
+            if (w1) acc[r] = nh_acc(acc[r], x1, klo[i][r + 1], khi[i][r + 1]);
+          }
         }
       }
+      const u64 tot = half_reduce_scatter<K>(acc, g);
+      const u64 s = 2 * pr + half;
+      if ((g & (16 / KP - 1)) == 0 && myidx < K && s < P.n_strings) P.out[s * K + myidx] = tot + P.tag[myidx];
     }
-    const u64 tot = half_reduce_scatter<K>(acc, g);
-    const u64 s = 2 * pr + half;
-    if ((g & (16 / KP - 1)) == 0 && myidx < K && s < P.n_strings) P.out[s * K + myidx] = tot + P.tag[myidx];
+    cseq++;
   }
 }
 

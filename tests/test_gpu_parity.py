@@ -109,6 +109,31 @@ def test_tail_only_kernel(hh, w):
 
 
 @pytest.mark.parametrize("w", VARIANTS)
+def test_small_string_kernel(hh, w):
+    # 1..7 instances with 8-byte-aligned strides take the packed small-string
+    # kernel (G = 4/2/1 strings per stage by stride); partial final words in
+    # the tail, batch sizes not a multiple of G, and the strides just inside
+    # and outside its packing limit (stride <= n + 256)
+    v = o.variant(w)
+    iw = v.m * 8
+    for inst in range(1, 8):
+        for tail in (0, 8, 13, iw - 1):
+            n = inst * iw + tail
+            a8 = (n + 7) // 8 * 8
+            for stride, count in ((a8, 33), (a8 + 8, 5), ((n + 15) // 16 * 16, 3), (a8 + 256, 7), (a8 + 264, 2)):
+                if stride >= n:
+                    _check_fixed(hh, w, count, n, stride=stride)
+    # batches large enough for 4 and 2 strings per stage (odd counts)
+    _check_fixed(hh, w, 12001, iw + 13)
+    _check_fixed(hh, w, 6001, 3 * iw + 8)
+    _check_fixed(hh, w, 12003, 2 * iw, stride=2 * iw + 24)
+    # the partial final word inside the last instance (job-kernel path)
+    _check_fixed(hh, w, 9, 3 * iw - 3, stride=3 * iw)
+    _check_fixed(hh, w, 1001, 2 * iw + 40)
+    _check_fixed(hh, w, 1, 5 * iw + 77)
+
+
+@pytest.mark.parametrize("w", VARIANTS)
 def test_multi_job_and_tree_levels(hh, w):
     # job boundaries (64 instances), level-2 / level-3 merges, powers of 8 +- 1
     v = o.variant(w)
@@ -144,6 +169,28 @@ def test_varlen_packed(hh, w):
     want = coracle.hash_varlen(w, host, off, S)
     bad = np.nonzero(~np.all(got == want, axis=1))[0]
     assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]} offsets {off[bad[:8]] % 16}"
+
+
+@pytest.mark.parametrize("n_strings", (16384, 16385, 70001))
+def test_varlen_plan_paths(hh, n_strings):
+    # up to 16384 strings are planned by one block (plan_one_kernel), more by
+    # the count / device-scan / scatter kernels; both must give the same digests
+    from workloads import offsets_of
+
+    rng = np.random.default_rng(n_strings)
+    lengths = rng.integers(0, 2500, n_strings).astype(np.uint64)
+    lengths[::1009] = 70000 + rng.integers(0, 9000, len(lengths[::1009]))
+    off = offsets_of(lengths)
+    total = int(off[-1])
+    buf = hh.fill_bytes(total, 9)
+    host = np.frombuffer(o.fill_bytes(total, 9), dtype=np.uint8).copy()
+    for w in (24, 40):
+        p = hh.variant(w)
+        seed = hh.seed_for_input(bytes(range(32)), p, int(lengths.max()))
+        got = _u64(hh.hash_varlen(buf, off, seed, p))
+        want = coracle.hash_varlen(w, host, off, seed.words_np(0, seed.capacity))
+        bad = np.nonzero(~np.all(got == want, axis=1))[0]
+        assert bad.size == 0, f"v{w}: {bad.size} mismatches, first {bad[:8]}"
 
 
 @pytest.mark.parametrize("w", (16, 40))
