@@ -357,7 +357,7 @@ def e2e_fixed(hh, torch, workload, steps, n_strings_cap=None, rank=0, world=1, l
     dt = statistics.median(times)
     return {"value": world * B * n / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": world * B * n,
             "d2h_bytes_per_step": world * B * p.output_words * 8, "strings_per_step": world * B,
-            "steps": steps, "api": "hth_hash_fixed_host (pinned host memory, 3-stream chunked H2D/hash/D2H), "
+            "steps": steps, "api": "hth_hash_fixed_host (pinned host memory, 3-stream chunked H2D/hash, one D2H of the digests), "
                                    "all ranks concurrently, max-over-ranks wall time"}, out
 
 

@@ -219,6 +219,12 @@ __host__ __device__ __forceinline__ u64 queue_cap(int c, u64 max_jobs, u64 q_ins
   return c == 0 ? 0 : min(max_jobs, q_inst / (u64)c + 1);
 }
 
+// Zero-slot finalize sums (tree.py:103-134): for a layout with L levels,
+// level l and digit d = (n_inst >> 3l) & 7 the empty slots d..6 contribute
+//   Z[L][l][d][r] = sum_{slot=d..6} sum_j NH(0, S[F_r(L) + 56 l + 8 slot + j]),
+// stored for L = 1..lmax at ztab_base(L) + (l * 8 + d) * K + r.
+__host__ __device__ __forceinline__ u64 ztab_base(u32 L, int K) { return 4ull * K * L * (L - 1); }
+
 struct Params {
   const uint8_t* data;
   u64 n_strings;
@@ -232,6 +238,8 @@ struct Params {
   const u64* job_map;  // varlen: per-size-class job queues of (string | job index in string << 32)
   const u64* meta;     // varlen: 2 u64 per string (scratch, counter bases; multi-job strings)
   const u32* cls_cnt;  // varlen: jobs per size class (plan_queue_kernel)
+  const u64* ztab;     // varlen: zero-slot finalize sums per (levels, level, digit, row)
+  u32 ztab_lmax;       // varlen: levels covered by ztab
   const u64* S;        // expanded seed words (SeedBuffer.words_np)
   const u64* folds;    // PERSEED: per-string seed folds
   u64* out;

@@ -142,62 +142,129 @@ __global__ void fill_kernel(u64 seed, u64 woff, u64 n_words, u64 n_bytes, u64* d
   }
 }
 
-// Varlen plan (one kernel): per string its instance count; strings shorter
-// than one instance go to the tail list (tail_varlen_kernel), every other
-// string's jobs are appended to the queue of their size class (min(instances,
-// 64)); the hash kernel claims classes largest first (LPT scheduling with
-// dynamic claiming).  Queue order inside a class and the scratch/counter
-// bases of multi-job strings come from atomics: digests are integer sums and
-// do not depend on them.  err bit 1: a string longer than max_n; bit 2: more
-// instances than the declared total (queues would overflow; job dropped).
+// Varlen plan + short strings (one kernel).  One half-warp per string: lane
+// 0 plans it -- a string of >= 1 instance appends its jobs to the queue of
+// their size class (min(instances, 64)), which the hash kernel claims largest
+// class first (LPT scheduling with dynamic claiming) -- and a string shorter
+// than one instance is hashed right here by its 16 lanes:
+//   D_r = NH(n, S[F_r]) + sum_i NH(W_i, S[R + r + i])   (hasher.py:400-412)
+// with the Toeplitz keys staged in shared memory.  Queue order inside a class
+// and the scratch/counter bases of multi-job strings come from atomics:
+// digests are integer sums and do not depend on them.  The grid's first
+// threads also build the zero-slot table (ztab_base).  err bit 1: a string
+// longer than max_n; bit 2: more instances than the declared total (the
+// queues would overflow; the job is dropped).
 struct QueueTable {
   u64 qb[NCLS + 1];  // queue c occupies job_map[qb[c], qb[c+1])
 };
+struct PlanParams {
+  const uint8_t* data;
+  const u64* off;
+  u64 n, max_n;
+  int job_lvl;
+  u32 lmax;
+  const u64* S;
+  u64 R, F0;  // L' = 1 layout: remainder start, finalize start of row 0 (row stride 64)
+  u64* out;
+  int* err;
+  u32* cls_cnt;
+  u64* queues;
+  u64* meta;
+  unsigned long long* totals;
+  u64* ztab;
+  QueueTable Q;
+};
 template <int OUT>
-__global__ void __launch_bounds__(256) plan_queue_kernel(const u64* off, u64 n, u64 max_n, int job_lvl,
-                                                         const __grid_constant__ QueueTable Q, int* err, u32* cls_cnt,
-                                                         u64* queues, u64* meta, unsigned long long* totals,
-                                                         u32* tail_list, u32* tail_count) {
-  constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m;
-  const int lane = threadIdx.x & 31;
-  const u64 per = 1ull << (3 * job_lvl);
-  const u64 step = (u64)gridDim.x * blockDim.x;
-  // whole warps iterate together so the tail-list append can be aggregated
-  for (u64 s0 = (u64)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); s0 < n; s0 += step) {
-    const u64 s = s0 + lane;
-    u64 ni = 0;
-    bool tail = false;
-    if (s < n) {
-      u64 nb = off[s + 1] - off[s];
-      if (nb > max_n) {
-        atomicOr(err, 1);
-        nb = max_n;
-      }
-      ni = ((nb + 7) >> 3) / M;
-      tail = ni == 0;
-    }
-    const unsigned tm = __ballot_sync(0xffffffffu, tail);
-    u32 tb = 0;
-    if (lane == 0 && tm) tb = atomicAdd(tail_count, (u32)__popc(tm));
-    tb = __shfl_sync(0xffffffffu, tb, 0);
-    if (tail) tail_list[tb + __popc(tm & ((1u << lane) - 1))] = (u32)s;
-    if (s >= n || tail) continue;
-    const u64 J = job_count(ni, job_lvl);
-    u64 w, c;
-    scratch_need(ni, K, job_lvl, &w, &c);
-    meta[2 * s] = w ? atomicAdd(totals, (unsigned long long)w) : 0;
-    meta[2 * s + 1] = c ? atomicAdd(totals + 1, (unsigned long long)c) : 0;
-    for (u64 q = 0; q < J; q++) {
-      const u64 jn = min(per, ni - q * per);
-      const int cl = jn > 64 ? 64 : (int)jn;
-      const u32 pos = atomicAdd(cls_cnt + cl, 1u);
-      if (pos < Q.qb[cl + 1] - Q.qb[cl]) {
-        queues[Q.qb[cl] + pos] = s | (q << 32);
-      } else {
-        atomicSub(cls_cnt + cl, 1u);
-        atomicOr(err, 2);
+__global__ void __launch_bounds__(256) plan_tail_kernel(const __grid_constant__ PlanParams P) {
+  constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m, EW = Geo<Var<OUT>>::ew;
+  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
+  constexpr int NKEY = M + K;  // Toeplitz keys R .. R + m + k - 2, plus slack
+  __shared__ u64 key[NKEY];
+  __shared__ u64 tagseed[K];
+  for (int i = threadIdx.x; i < NKEY; i += blockDim.x) key[i] = __ldg(P.S + P.R + i);
+  if (threadIdx.x < K) tagseed[threadIdx.x] = __ldg(P.S + P.F0 + 64ull * threadIdx.x);
+  // zero-slot table: one thread per (L, l, r) sums its 7 slots and writes the
+  // suffix sums for digits 0..7
+  const u64 nz = (u64)K * P.lmax * P.lmax;
+  for (u64 x = (u64)blockIdx.x * blockDim.x + threadIdx.x; x < nz; x += (u64)gridDim.x * blockDim.x) {
+    const u32 r = (u32)(x % K), l = (u32)(x / K % P.lmax), L = (u32)(x / K / P.lmax) + 1;
+    if (l >= L) continue;
+    const u64 F = (u64)EW + 7ull * L * K + 64ull * L * r + 56ull * l;  // seed_layout (hasher.py:130-153)
+    u64* z = P.ztab + ztab_base(L, K) + (u64)l * 8 * K + r;
+    u64 part[7];  // all 56 seed loads in flight at once
+#pragma unroll
+    for (int slot = 0; slot < 7; slot++) {
+      part[slot] = 0;
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const u64 sw = __ldg(P.S + F + 8 * slot + j);
+        part[slot] += (u64)(u32)sw * (u64)(u32)(sw >> 32);  // NH(0, s)
       }
     }
+    u64 acc = 0;
+    z[7 * K] = 0;
+#pragma unroll
+    for (int slot = 6; slot >= 0; slot--) {
+      acc += part[slot];
+      z[slot * K] = acc;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane & 15;
+  const int myidx = scatter_index<K>(g);
+  const u64 per = 1ull << (3 * P.job_lvl);
+  const u64 halves = (u64)gridDim.x * (blockDim.x >> 4);
+  // both halves of a warp iterate together (the reduction shuffles are warp-wide)
+  for (u64 s = (u64)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); s < ((P.n + 1) & ~1ull); s += halves) {
+    const bool live = s < P.n;
+    const u64 o0 = live ? P.off[s] : 0;
+    u64 n = live ? P.off[s + 1] - o0 : 0;
+    if (n > P.max_n) {
+      if (g == 0) atomicOr(P.err, 1);
+      n = P.max_n;
+    }
+    const u64 ni = ((n + 7) >> 3) / M;
+    const bool tail = live && ni == 0;
+    if (live && !tail && g == 0) {
+      const u64 J = job_count(ni, P.job_lvl);
+      u64 w, c;
+      scratch_need(ni, K, P.job_lvl, &w, &c);
+      P.meta[2 * s] = w ? atomicAdd(P.totals, (unsigned long long)w) : 0;
+      P.meta[2 * s + 1] = c ? atomicAdd(P.totals + 1, (unsigned long long)c) : 0;
+      for (u64 q = 0; q < J; q++) {
+        const u64 jn = min(per, ni - q * per);
+        const int cl = jn > 64 ? 64 : (int)jn;
+        const u32 pos = atomicAdd(P.cls_cnt + cl, 1u);
+        if (pos < P.Q.qb[cl + 1] - P.Q.qb[cl]) {
+          P.queues[P.Q.qb[cl] + pos] = s | (q << 32);
+        } else {
+          atomicSub(P.cls_cnt + cl, 1u);
+          atomicOr(P.err, 2);
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, tail)) continue;
+    u64 acc[K];
+#pragma unroll
+    for (int r = 0; r < K; r++) acc[r] = 0;
+    const u32 nw = tail ? (u32)((n + 7) >> 3) : 0;
+    for (u32 t = g; t < nw; t += 16) {
+      const u64 b = o0 + 8ull * t;
+      const u64* p = reinterpret_cast<const u64*>(P.data + (b & ~7ull));
+      const u32 sh = (u32)(b & 7) * 8;
+      u64 x = __ldg(p);
+      if (sh) x = (x >> sh) | (__ldg(p + 1) << (64 - sh));
+      const u64 rem = n - 8ull * t;
+      if (rem < 8) x &= (1ull << (8 * rem)) - 1;  // zero-pad the partial last word (hasher.py:179-183)
+#pragma unroll
+      for (int r = 0; r < K; r++) acc[r] = nh_acc(acc[r], x, key[t + r]);
+    }
+    if (g == 0 && tail) {
+#pragma unroll
+      for (int r = 0; r < K; r++) acc[r] = nh_acc(acc[r], n, tagseed[r]);  // finalize over the tag
+    }
+    const u64 tot = half_reduce_scatter<K>(acc, g);
+    if (tail && (g & (16 / KP - 1)) == 0 && myidx < K) P.out[s * K + myidx] = tot;
   }
 }
 
@@ -437,15 +504,18 @@ FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
 
 // varlen workspace geometry
 struct VarPlan {
-  u64 off_err, off_cnt, off_acc, off_ev, off_ctl, off_pctl, off_clear, off_tail, off_meta, off_queue, off_scr, total,
-      max_jobs, q_inst, scr_words, cnts;
+  u64 off_err, off_cnt, off_acc, off_ev, off_ctl, off_pctl, off_clear, off_meta, off_queue, off_scr, total,
+      max_jobs, q_inst, scr_words, cnts, off_ztab, lmax;
   QueueTable Q;
 };
 // Workspace: the error flag (offset 0, hth_varlen_status), the self-resetting
 // hash state and the plan counters first (cleared by one memset per call),
-// then the tail list, per-string bases, class queues and merge scratch.
-int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
+// then the per-string bases, class queues, merge scratch and zero-slot table.
+int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPlan* p) {
   const u64 total_inst = total_bytes / (8ull * v.m);
+  // no string has more levels than the longest allowed one, nor than the total
+  const u64 max_inst = std::min(((max_n_bytes / 8) + 1) / (u64)v.m, total_inst);
+  p->lmax = max_inst ? level_count(max_inst) : 1;
   p->max_jobs = n + total_inst / 64 + 1;
   p->q_inst = total_inst;
   p->scr_words = (total_inst / 56 + 1) * 8ull * v.k;
@@ -462,12 +532,12 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, VarPlan* p) {
   p->off_acc = o; o = align_up(o + n * v.k * 8, 256);
   p->off_ev = o; o = align_up(o + n * 4, 256);
   p->off_ctl = o; o += 256;
-  p->off_pctl = o; o += 512;  // class counts [NCLS] u32 @0, tail count @320, scratch/counter totals @384
+  p->off_pctl = o; o += 512;  // class counts [NCLS] u32 @0, scratch/counter totals @384
   p->off_clear = o;
-  p->off_tail = o; o = align_up(o + n * 4, 256);
   p->off_meta = o; o = align_up(o + n * 16, 256);
   p->off_queue = o; o = align_up(o + qcap * 8, 256);
   p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
+  p->off_ztab = o; o = align_up(o + ztab_base(p->lmax + 1, v.k) * 8, 256);
   p->total = o;
   return HTH_OK;
 }
@@ -710,7 +780,7 @@ int hth_workspace_size_varlen(int output_bytes, uint64_t n_strings, uint64_t tot
   if (int rc = get_var(output_bytes, &v)) return rc;
   if (!bytes) return fail(HTH_EINVAL, "null output pointer");
   VarPlan p;
-  if (int rc = varlen_plan(v, n_strings, total_bytes, &p)) return rc;
+  if (int rc = varlen_plan(v, n_strings, total_bytes, ~0ull, &p)) return rc;
   *bytes = p.total;
   return HTH_OK;
 }
@@ -727,7 +797,7 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   if (reinterpret_cast<uintptr_t>(d_data) & 15) return fail(HTH_EINVAL, "d_data must be 16-byte aligned");
   if (n_strings >= (1ull << 32)) return fail(HTH_EINVAL, "at most 2^32-1 strings per call");
   VarPlan p;
-  if (int rc = varlen_plan(v, n_strings, total_bytes, &p)) return rc;
+  if (int rc = varlen_plan(v, n_strings, total_bytes, max_n_bytes, &p)) return rc;
   if (workspace_bytes < p.total)
     return fail(HTH_EINVAL, "workspace too small: %llu < %llu bytes", (unsigned long long)workspace_bytes,
                 (unsigned long long)p.total);
@@ -735,52 +805,47 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   uint8_t* ws = (uint8_t*)d_workspace;
   int* err = (int*)(ws + p.off_err);
   u32* cls_cnt = (u32*)(ws + p.off_pctl);
-  u32* tail_count = (u32*)(ws + p.off_pctl + 320);
   auto* totals = (unsigned long long*)(ws + p.off_pctl + 384);
-  u32* tail_list = (u32*)(ws + p.off_tail);
-  u64* meta = (u64*)(ws + p.off_meta);
-  u64* queues = (u64*)(ws + p.off_queue);
   // plan areas of an earlier call may overlap this call's counters/accumulators
   CK(cudaMemsetAsync(ws, 0, p.off_clear, st));
   const int job_lvl = pick_job_lvl(((max_n_bytes + 7) / 8) / (u64)v.m);
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  const unsigned pb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 256), (u64)sm_count(dev) * 8));
+  PlanParams Q{};
+  Q.data = (const uint8_t*)d_data;
+  Q.off = d_offsets;
+  Q.n = n_strings;
+  Q.max_n = max_n_bytes;
+  Q.job_lvl = job_lvl;
+  Q.lmax = (u32)p.lmax;
+  Q.S = d_seed;
+  Q.R = (u64)v.ew + 71ull * v.k;  // L' = 1 layout (hasher.py:130-153)
+  Q.F0 = (u64)v.ew + 7ull * v.k;
+  Q.out = d_out;
+  Q.err = (int*)(ws + p.off_err);
+  Q.cls_cnt = cls_cnt;
+  Q.queues = (u64*)(ws + p.off_queue);
+  Q.meta = (u64*)(ws + p.off_meta);
+  Q.totals = totals;
+  Q.ztab = (u64*)(ws + p.off_ztab);
+  Q.Q = p.Q;
+  const unsigned pb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 16), (u64)sm_count(dev) * 16));
   switch (output_bytes) {
-    case 16: plan_queue_kernel<16><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
-    case 24: plan_queue_kernel<24><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
-    case 32: plan_queue_kernel<32><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
-    case 40: plan_queue_kernel<40><<<pb, 256, 0, st>>>(d_offsets, n_strings, max_n_bytes, job_lvl, p.Q, err, cls_cnt, queues, meta, totals, tail_list, tail_count); break;
+    case 16: plan_tail_kernel<16><<<pb, 256, 0, st>>>(Q); break;
+    case 24: plan_tail_kernel<24><<<pb, 256, 0, st>>>(Q); break;
+    case 32: plan_tail_kernel<32><<<pb, 256, 0, st>>>(Q); break;
+    case 40: plan_tail_kernel<40><<<pb, 256, 0, st>>>(Q); break;
   }
   CK(cudaGetLastError());
-  {
-    TailVarParams T{};
-    T.data = (const uint8_t*)d_data;
-    T.offsets = d_offsets;
-    T.list = tail_list;
-    T.count = tail_count;
-    T.max_n = max_n_bytes;
-    T.S = d_seed;
-    T.R = (u64)v.ew + 71ull * v.k;  // L' = 1 layout (hasher.py:130-153)
-    T.F0 = (u64)v.ew + 7ull * v.k;
-    T.Fstep = 64;
-    T.out = d_out;
-    const unsigned tb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 16), (u64)sm_count(dev) * 8));
-    switch (output_bytes) {
-      case 16: tail_varlen_kernel<16><<<tb, 256, 0, st>>>(T); break;
-      case 24: tail_varlen_kernel<24><<<tb, 256, 0, st>>>(T); break;
-      case 32: tail_varlen_kernel<32><<<tb, 256, 0, st>>>(T); break;
-      case 40: tail_varlen_kernel<40><<<tb, 256, 0, st>>>(T); break;
-    }
-    CK(cudaGetLastError());
-  }
   Params P{};
   P.data = (const uint8_t*)d_data;
   P.n_strings = n_strings;
   P.offsets = d_offsets;
-  P.job_map = queues;
-  P.meta = meta;
+  P.job_map = Q.queues;
+  P.meta = Q.meta;
   P.cls_cnt = cls_cnt;
+  P.ztab = (const u64*)(ws + p.off_ztab);
+  P.ztab_lmax = (u32)p.lmax;
   P.n_jobs = p.max_jobs;  // varlen: queue sizing bound; the kernel counts the jobs itself
   memcpy(P.cls_qb, p.Q.qb, sizeof(P.cls_qb));
   P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_queue_kernel)
@@ -960,9 +1025,16 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
     if (int rc = hth_hash_fixed(output_bytes, c->buf[b], ns, dstride, n_bytes, fold_of(master), c->seeds, lay.total,
                                 c->out + s0 * v.k, c->ws[b], c->ws_bytes, st))
       return rc;
-    CK(cudaMemcpyAsync(h_out + s0 * v.k, c->out + s0 * v.k, ns * v.k * 8, cudaMemcpyDeviceToHost, st));
   }
-  for (int i = 0; i < 3; i++) CK(cudaStreamSynchronize(c->st[i]));
+  // digests stay on the device until every chunk is hashed: a per-chunk copy
+  // into (pageable) h_out blocks this thread until that chunk's kernel ends,
+  // which starves the copy engine of the next chunk (~0.1 ms gap per chunk)
+  for (int i = 1; i < 3; i++) {
+    CK(cudaEventRecord(seeded, c->st[i]));
+    CK(cudaStreamWaitEvent(c->st[0], seeded, 0));
+  }
+  CK(cudaMemcpyAsync(h_out, c->out, n_strings * v.k * 8, cudaMemcpyDeviceToHost, c->st[0]));
+  CK(cudaStreamSynchronize(c->st[0]));
   cudaEventDestroy(seeded);
   return HTH_OK;
 }

@@ -285,7 +285,6 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     __syncthreads();
     n_jobs = cls_pre[0];
   }
-  int ccur = NCLS - 1;  // varlen: class of this warp's latest claim (ids only grow)
   u32 qhead = 0, qtail = 0;        // queue: [qtail, qhead) claimed, not yet started
   bool pdone = false;
   // the first job of every warp is static (job = global warp index), so the
@@ -316,7 +315,14 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     }
     u64 e = jc;
     if (VARLEN) {  // job id -> class queue entry
-      while (jc >= cls_pre[ccur - 1]) ccur--;
+      // the smallest class c with cls_pre[c] <= jc (cls_pre falls as c grows)
+      int lo = 1, hi = NCLS - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cls_pre[mid] <= jc) hi = mid;
+        else lo = mid + 1;
+      }
+      const int ccur = lo;
       e = P.job_map[P.cls_qb[ccur] + (jc - cls_pre[ccur])];
     }
     if (lane == 0) jq_buf[qhead % QN] = e;
@@ -543,6 +549,18 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       if (lane == 0) {
 #pragma unroll
         for (int r = 0; r < K; r++) fin[r] += P.fin_const[r];
+      }
+    } else if (last_job && VARLEN && st.n_inst && st.L <= P.ztab_lmax) {
+      // zero-slot sums from the plan's table (zero_slot_table), then the tag
+      if (lane == 0) {
+        const u64* z = P.ztab + ztab_base(st.L, K);
+        for (u32 l = 0; l < st.L; l++) {
+          const u64* zl = z + (l * 8 + ((st.n_inst >> (3 * l)) & 7)) * K;
+#pragma unroll
+          for (int r = 0; r < K; r++) fin[r] += zl[r];
+        }
+#pragma unroll
+        for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, sd(tc.F(r) + 56u * st.L));
       }
     } else if (last_job) {
       // zero slots and the length tag of the finalize NH (hasher.py:387-405)

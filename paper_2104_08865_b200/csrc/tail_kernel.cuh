@@ -184,69 +184,3 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
 }
 
 }  // namespace hth
-
-namespace hth {
-
-// Variable-length batches: the strings shorter than one instance (the bulk of
-// config 2's strings) skip the job machinery.  A half-warp hashes one string
-// straight from global memory (any byte alignment: two aligned 8-byte loads
-// and a funnel shift per word); the Toeplitz keys S[R..R+m+k) and the tag
-// seeds S[F_r] -- shared by every such string (layout L' = 1) -- are staged
-// in shared memory once per CTA.
-struct TailVarParams {
-  const uint8_t* data;
-  const u64* offsets;
-  const u32* list;  // tail-only string indices
-  const u32* count; // number of entries in list
-  u64 max_n;        // length clamp (host-checked bound)
-  const u64* S;
-  u64 R, F0, Fstep;  // remainder start, finalize start of row 0, row stride (L' = 1)
-  u64* out;
-};
-
-template <int OUT>
-__global__ void __launch_bounds__(256) tail_varlen_kernel(const __grid_constant__ TailVarParams P) {
-  constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m;
-  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
-  constexpr int NKEY = M + K;  // keys R .. R + m + k - 2, plus slack
-  __shared__ u64 key[NKEY];
-  __shared__ u64 tagseed[K];
-  for (int i = threadIdx.x; i < NKEY; i += blockDim.x) key[i] = __ldg(P.S + P.R + i);
-  if (threadIdx.x < K) tagseed[threadIdx.x] = __ldg(P.S + P.F0 + P.Fstep * threadIdx.x);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, g = lane & 15, half = lane >> 4;
-  const u32 cnt = *P.count;
-  const u64 halves = (u64)gridDim.x * (blockDim.x >> 4);
-  const int myidx = scatter_index<K>(g);
-  for (u64 h = (u64)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); h < ((cnt + 1ull) & ~1ull);
-       h += halves) {
-    // both halves of a warp iterate together (shuffles are warp-wide)
-    const bool live = h < cnt;
-    const u32 s = live ? P.list[h] : 0;
-    const u64 o0 = live ? P.offsets[s] : 0;
-    const u64 n = live ? min(P.offsets[s + 1] - o0, P.max_n) : 0;
-    const u32 nw = (u32)((n + 7) >> 3);
-    u64 acc[K];
-#pragma unroll
-    for (int r = 0; r < K; r++) acc[r] = 0;
-    for (u32 t = g; t < nw; t += 16) {
-      const u64 b = o0 + 8ull * t;
-      const u64* p = reinterpret_cast<const u64*>(P.data + (b & ~7ull));
-      const u32 sh = (u32)(b & 7) * 8;
-      u64 x = __ldg(p);
-      if (sh) x = (x >> sh) | (__ldg(p + 1) << (64 - sh));
-      const u64 rem = n - 8ull * t;
-      if (rem < 8) x &= (1ull << (8 * rem)) - 1;  // zero-pad the partial last word
-#pragma unroll
-      for (int r = 0; r < K; r++) acc[r] = nh_acc(acc[r], x, key[t + r]);
-    }
-    if (g == 0 && live) {
-#pragma unroll
-      for (int r = 0; r < K; r++) acc[r] = nh_acc(acc[r], n, tagseed[r]);  // finalize over the tag
-    }
-    const u64 tot = half_reduce_scatter<K>(acc, g);
-    if (live && (g & (16 / KP - 1)) == 0 && myidx < K) P.out[(u64)s * K + myidx] = tot;
-  }
-}
-
-}  // namespace hth
