@@ -123,19 +123,35 @@ class ClockSampler:
 _CPU_SAMPLE = {}
 
 
-def _cpu_task(i):
-    """Hash worker i's pre-generated strings with the numpy oracle (inherited via fork)."""
+def _cpu_task(arg):
+    """Hash worker i's next `count` pre-generated strings (from `start`, cyclic)
+    with the numpy oracle (the pool is inherited via fork)."""
     from oracle import oracle_np as o
 
-    v, n, S, words = _CPU_SAMPLE["v"], _CPU_SAMPLE["n"], _CPU_SAMPLE["S"], _CPU_SAMPLE["words"][i]
+    i, start, count = arg
+    v, n, S, pool = _CPU_SAMPLE["v"], _CPU_SAMPLE["n"], _CPU_SAMPLE["S"], _CPU_SAMPLE["words"][i]
+    if start + count <= pool.shape[0]:
+        words = pool[start:start + count]
+    else:
+        words = pool[(start + np.arange(count)) % pool.shape[0]]
     o.hash_batch(v, words, n, S)
-    return words.shape[0] * n
+    return count * n
+
+
+# strings per core per pass of the CPU arm (~4 MiB: the numpy port's best granularity)
+CPU_PER_CORE = {"cfg1": 1024, "cfg3": 4096, "cfg4": 4, "cfg5": 1}
+
+# per-core pool of distinct strings, larger than the last-level cache share,
+# so every pass streams fresh data from DRAM as the reference would
+CPU_POOL_BYTES = 64 << 20
 
 
 class CpuBaseline:
     """The reference's CPU algorithm (numpy restatement of hasher.py:331-413)
-    on `cores` forked processes; each holds `per_core` strings of the workload,
-    generated before any timing.  rate() times one pass over all of them."""
+    on `cores` forked processes.  Each process holds a pool of >= 64 MiB of
+    distinct strings of the workload, generated before any timing; rate()
+    times one pass in which every process hashes its next `per_core` strings
+    (cyclic), so small samples are not served from cache."""
 
     def __init__(self, workload: str, per_core: int, cores: int):
         from oracle import oracle_np as o
@@ -145,25 +161,31 @@ class CpuBaseline:
         if workload == "cfg5":  # one huge string: time 16 MiB pieces of it
             n = 16 << 20
         v = o.variant(w)
+        assert n % 8 == 0
+        per_pool = max(per_core, -(-CPU_POOL_BYTES // n))
         _CPU_SAMPLE.update(v=v, n=n, S=o.splitmix_words(o.master_fold(wl.MASTER), 0, o.seed_words_needed(v, n)))
         _CPU_SAMPLE["words"] = [
-            np.stack([o.words_from_bytes(wl.host_bytes((i * per_core + t) * n, n)) for t in range(per_core)])
+            o.words_from_bytes(wl.host_bytes(i * per_pool * n, per_pool * n)).reshape(per_pool, -1)
             for i in range(cores)]
-        self.cores, self.per_core, self.n, self.w = cores, per_core, n, w
+        self.cores, self.per_core, self.n, self.w, self.per_pool = cores, per_core, n, w, per_pool
+        self.next = 0
         self.pool = mp.get_context("fork").Pool(cores) if cores > 1 else None
 
     def rate(self):
+        args = [(i, self.next, self.per_core) for i in range(self.cores)]
+        self.next = (self.next + self.per_core) % self.per_pool
         t0 = time.perf_counter()
         if self.pool is None:
-            total = _cpu_task(0)
+            total = _cpu_task(args[0])
         else:
-            total = sum(self.pool.map(_cpu_task, range(self.cores), chunksize=1))
+            total = sum(self.pool.map(_cpu_task, args, chunksize=1))
         dt = time.perf_counter() - t0
         return total / dt / 1e9, total, dt
 
     def sample(self):
         return (f"{self.cores} processes x {self.per_core} strings of {self.n} B (v{self.w}) per pass, "
-                "data pre-generated; numpy restatement of hasher.py:331-413 (oracle/oracle_np.py, "
+                f"each from its own pool of {self.per_pool} distinct pre-generated strings (cyclic, larger "
+                "than the caches); numpy restatement of hasher.py:331-413 (oracle/oracle_np.py, "
                 "bit-identical to the reference, ~1.3x its single-core speed)")
 
     def close(self):
@@ -367,7 +389,7 @@ def arm_reference(args, rank, world):
         return 0
     workload = args.workload
     cores = os.cpu_count() or 1
-    per_core = {"cfg1": 64, "cfg3": 256, "cfg4": 4, "cfg5": 1}.get(workload, 4)
+    per_core = CPU_PER_CORE.get(workload, 4)
     cpu = CpuBaseline(workload, per_core, cores)
     for _ in range(args.warmup):
         cpu.rate()
@@ -459,11 +481,15 @@ def arm_ours(args, rank, world, local_rank):
                 except Exception as ex:  # pragma: no cover
                     extra[wk] = {"error": repr(ex)}
         cores = os.cpu_count() or 1
-        cb = CpuBaseline(workload, 32, cores)  # ~0.4 s per core per pass
+        # the reference arm's granularity (the numpy port is fastest on small
+        # batches), median of several passes over fresh strings
+        cb = CpuBaseline(workload, CPU_PER_CORE.get(workload, 4), cores)
         cb.rate()
-        r, b, dt = cb.rate()
+        runs = [cb.rate() for _ in range(8)]
         cb.close()
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port", "sample": cb.sample() + f"; {dt:.2f} s"}
+        r = statistics.median(x[0] for x in runs)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": cb.sample() + f"; median of 8 passes, {sum(x[2] for x in runs):.2f} s"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
