@@ -10,9 +10,11 @@ The kernel packs plane b of the same word position of TWO instances into one
 32-bit register (instance A in the low half, B in the high half), so one
 32-bit XOR advances 2 x 16 GF(16) elements.  This script emits, per variant,
 the straight-line XOR schedule of all parity planes from all input planes,
-with common subexpressions shared (greedy Paar elimination), single-use
-shared terms inlined, and every XOR chain emitted as explicit 3-input LOP3s
-(ptxas alone left ~15 % of them as 2-input).
+with common pairs and triples of terms shared (a seeded randomised greedy
+search costed directly in 3-input LOP3s: 33/47/47 LOP3 per block pair for
+v24/v32/v40, against 40/64/62 from plain greedy Paar elimination), and every
+XOR chain emitted as explicit 3-input LOP3s (ptxas alone left ~15 % of them
+as 2-input).
 
 Run:  python gen_encode.py > encode_gen.cuh
 """
@@ -57,34 +59,8 @@ def cauchy(d, p):  # params.py:115-130
 VARIANTS = {24: (7, cauchy(7, 2)), 32: (7, cauchy(7, 3)), 40: (5, cauchy(5, 4))}
 
 
-def paar(rows, nin):
-    """Greedy Paar CSE. rows: list of sets of input ids. Returns (temps, rows)."""
-    rows = [set(r) for r in rows]
-    temps = []
-    nxt = nin
-    while True:
-        cnt = {}
-        for r in rows:
-            rl = sorted(r)
-            for i in range(len(rl)):
-                for j in range(i + 1, len(rl)):
-                    cnt[(rl[i], rl[j])] = cnt.get((rl[i], rl[j]), 0) + 1
-        if not cnt:
-            break
-        (a, b), c = max(cnt.items(), key=lambda kv: (kv[1], -kv[0][0], -kv[0][1]))
-        if c < 2:
-            break
-        temps.append((nxt, a, b))
-        for r in rows:
-            if a in r and b in r:
-                r.discard(a)
-                r.discard(b)
-                r.add(nxt)
-        nxt += 1
-    return temps, rows
-
-
 def parity_rows(d, P):
+    """Output plane (p, a) as the set of input planes 4 i + b it XORs."""
     rows = []
     for p in range(len(P)):
         for a in range(4):
@@ -98,35 +74,73 @@ def parity_rows(d, P):
     return rows
 
 
-def lop3_program(d, P):
-    """Paar-shared temps; temps used once are inlined into their consumer;
-    every XOR of n terms becomes ceil((n-1)/2) 3-input XORs (LOP3 0x96)."""
-    temps, rows = paar(parity_rows(d, P), 4 * d)
-    uses = {}
-    for (_, a, b) in temps:
-        uses[a] = uses.get(a, 0) + 1
-        uses[b] = uses.get(b, 0) + 1
-    for r in rows:
-        for v in r:
-            uses[v] = uses.get(v, 0) + 1
-    tdef = {t: (a, b) for t, a, b in temps}
-    mat = [t for t, _, _ in temps if uses.get(t, 0) >= 2]
+def lop3_cost(m):
+    """3-input LOP3s for an XOR of m terms."""
+    return max(0, m // 2) if m > 1 else 0
 
-    def expand(v):
-        if v in tdef and v not in mat:
-            a, b = tdef[v]
-            return expand(a) + expand(b)
-        return [v]
 
-    prog = []  # (dest, [terms]) in dependency order
-    for t in mat:
-        a, b = tdef[t]
-        prog.append((f"t{t}", expand(a) + expand(b)))
-    for k, r in enumerate(rows):
-        terms = []
-        for v in sorted(r):
-            terms += expand(v)
-        prog.append((f"y[{k}]", terms))
+def share_search(rows0, nin, rng, topk, triples):
+    """Randomised greedy common-subexpression sharing, costed in 3-input LOP3s.
+
+    Repeatedly picks (among the `topk` best) a pair or triple of terms that
+    occurs in >= 2 rows and whose replacement by one shared temp lowers the
+    total LOP3 count (temp: 1 LOP3; a row of m terms: ceil((m-1)/2)).
+    Returns (cost, temps [(id, terms)], rows)."""
+    import itertools
+
+    rows = [set(r) for r in rows0]
+    temps = []
+    nxt = nin
+    while True:
+        cnt = {}
+        for r in rows:
+            rl = sorted(r)
+            for k in itertools.combinations(rl, 2):
+                cnt[k] = cnt.get(k, 0) + 1
+            if triples and len(rl) <= 14:
+                for k in itertools.combinations(rl, 3):
+                    cnt[k] = cnt.get(k, 0) + 1
+        cands = []
+        for k, c in cnt.items():
+            if c < 2:
+                continue
+            ks = set(k)
+            gain = -1
+            for r in rows:
+                if ks <= r:
+                    gain += lop3_cost(len(r)) - lop3_cost(len(r) - len(k) + 1)
+            if gain > 0 or (gain == 0 and rng.random() < 0.1):
+                cands.append((gain, k))
+        if not cands:
+            break
+        cands.sort(key=lambda x: -x[0])
+        _, k = rng.choice(cands[:topk])
+        temps.append((nxt, k))
+        ks = set(k)
+        for r in rows:
+            if ks <= r:
+                r -= ks
+                r.add(nxt)
+        nxt += 1
+    return len(temps) + sum(lop3_cost(len(r)) for r in rows), temps, rows
+
+
+# best of 4000 seeded searches per variant (offline; see share_search)
+SEARCH_SEED = {24: 122, 32: 1869, 40: 3361}
+
+
+def lop3_program(d, P, seed=None):
+    """The parity XOR program: shared temps first, then the 4 * len(P) output
+    planes; each entry (dest, input/temp ids) is one XOR of its terms."""
+    import random
+
+    seed = SEARCH_SEED[{(7, 2): 24, (7, 3): 32, (5, 4): 40}[(d, len(P))]] if seed is None else seed
+    rng = random.Random(seed)
+    topk = rng.choice([1, 2, 3, 4])
+    triples = rng.random() < 0.8
+    _, temps, rows = share_search(parity_rows(d, P), 4 * d, rng, topk, triples)
+    prog = [(f"t{t}", list(k)) for t, k in temps]
+    prog += [(f"y[{i}]", sorted(r)) for i, r in enumerate(rows)]
     return prog
 
 
@@ -134,7 +148,7 @@ def emit(out_bytes, d, P):
     npar = len(P)
     prog = lop3_program(d, P)
     name = lambda v: f"x[{v}]" if v < 4 * d else f"t{v}"
-    n_lop = sum(max(0, (len(t) - 1 + 1) // 2) for _, t in prog)
+    n_lop = sum(lop3_cost(len(t)) for _, t in prog)
     lines = [f"// v{out_bytes}: {npar} parity words from {d} inputs: {n_lop} LOP3 per pair of blocks",
              f"__device__ __forceinline__ void enc_planes_{out_bytes}(const u32 (&x)[{4 * d}], u32 (&y)[{4 * npar}]) {{"]
     tmp = 0
