@@ -261,6 +261,40 @@ def make_flush(torch):
     return flush
 
 
+def measure_latency(hh, sizes=(64, 4096, 1 << 20, 64 << 20), variant=24, reps=20):
+    """Single-string latency of the public one-shot API (hash_bytes on host
+    bytes: seed expansion, H2D copy, hash, digest read-back),
+    wall clock, median of `reps` calls, beside the CPU port on one core."""
+    from oracle import oracle_np as o
+
+    p = hh.variant(variant)
+    v = o.variant(variant)
+    out = {"variant": variant, "api": "hash_bytes(bytes, SeedBuffer, params) -> Digest", "gpu_us": {}, "cpu_us": {}}
+    for n in sizes:
+        data = wl.host_bytes(0, n)
+        seed = hh.seed_for_input(wl.MASTER, p, n)
+        for _ in range(3):
+            d = hh.hash_bytes(data, seed, p)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            d = hh.hash_bytes(data, seed, p)
+            ts.append(time.perf_counter() - t0)
+        out["gpu_us"][str(n)] = round(statistics.median(ts) * 1e6, 1)
+        if n <= 1 << 20:
+            S = o.splitmix_words(o.master_fold(wl.MASTER), 0, o.seed_words_needed(v, n))
+            words = o.words_from_bytes(data).reshape(1, -1)
+            want = o.hash_batch(v, words, n, S)[0]
+            assert tuple(int(x) for x in want) == tuple(d.words), "latency probe digest mismatch"
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                o.hash_batch(v, words, n, S)
+                ts.append(time.perf_counter() - t0)
+            out["cpu_us"][str(n)] = round(statistics.median(ts) * 1e6, 1)
+    return out
+
+
 def measure_workload(hh, torch, workload, steps, warmup, peak):
     """N=1 secondary measurement of one config (rank 0 only)."""
     res = {"desc": wl.CONFIGS[workload]["desc"]}
@@ -480,6 +514,10 @@ def arm_ours(args, rank, world, local_rank):
                                                  peak=peak)
                 except Exception as ex:  # pragma: no cover
                     extra[wk] = {"error": repr(ex)}
+            try:
+                extra["latency"] = measure_latency(hh)
+            except Exception as ex:  # pragma: no cover
+                extra["latency"] = {"error": repr(ex)}
         cores = os.cpu_count() or 1
         # the reference arm's granularity (the numpy port is fastest on small
         # batches), median of several passes over fresh strings
