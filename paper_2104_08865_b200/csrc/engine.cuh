@@ -173,20 +173,25 @@ struct Str {
   u64 fold;          // PERSEED: this string's seed fold
 };
 
+// levels = 1 + floor(log8 n) for n >= 1 (tree.py:34-42)
 __host__ __device__ __forceinline__ u32 level_count(u64 n) {
+#ifdef __CUDA_ARCH__
+  return 1 + (u32)(63 - __clzll((long long)(n | 1))) / 3;
+#else
   u32 l = 1;
   while (n >= 8) {
     n >>= 3;
     l++;
   }
   return l;
+#endif
 }
 __host__ __device__ __forceinline__ u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
 
 // jobs of a string: one per 8^job_lvl instances (at least one)
 __host__ __device__ __forceinline__ u64 job_count(u64 n_inst, int job_lvl) {
   const u64 per = 1ull << (3 * job_lvl);
-  return n_inst > per ? ceil_div(n_inst, per) : 1;
+  return n_inst > per ? (n_inst + per - 1) >> (3 * job_lvl) : 1;  // per is a power of 8
 }
 
 // scratch words / counters a string needs for merges above the job level
@@ -235,7 +240,8 @@ struct Params {
   u64 scr_per;   // fixed mode: scratch words per string
   u64 cnt_per;   // fixed mode: counters per string
   const u64* offsets;  // varlen: n_strings + 1 byte offsets
-  const u64* job_map;  // varlen: per-size-class job queues of (string | job index in string << 32)
+  const u64* job_map;  // varlen: per-size-class job queues; each job a JOB_REC-word record
+                       // {byte offset, length, string | job index << 32, 0} (plan_tail_kernel)
   const u64* meta;     // varlen: 2 u64 per string (scratch, counter bases; multi-job strings)
   const u32* cls_cnt;  // varlen: jobs per size class (plan_queue_kernel)
   const u64* ztab;     // varlen: zero-slot finalize sums per (levels, level, digit, row)
@@ -281,18 +287,18 @@ __device__ __forceinline__ void layout_bases(u32 L, int ew, u64 (&T)[K], u64 (&F
   R = (u64)ew + 71ull * L * K;
 }
 
-// VARLEN: `job` is the queue entry (string | jq << 32) resolved at claim time
+constexpr int JOB_REC = 4;  // u64 words per varlen job record
+
+// VARLEN: `rec` is the job's record (queue entry), resolved at claim time;
+// fixed mode: `job` is the job index
 template <bool VARLEN, int K, int M>
-__device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u32& jq) {
+__device__ __forceinline__ void decode_job(const Params& P, u64 job, const u64* rec, Str& st, u32& jq) {
   u64 s;
   if (VARLEN) {
-    s = job & 0xffffffffull;
-    const u64 o0 = P.offsets[s], o1 = P.offsets[s + 1];
-    st.p = P.data + o0;
-    st.n = min(o1 - o0, P.n_bytes);  // clamp to the host-checked bound (plan_queue_kernel)
-    jq = (u32)(job >> 32);
-    st.scratch = P.meta[2 * s];
-    st.cnt = P.meta[2 * s + 1];
+    s = rec[2] & 0xffffffffull;
+    st.p = P.data + rec[0];
+    st.n = rec[1];  // clamped to the host-checked bound by plan_tail_kernel
+    jq = (u32)(rec[2] >> 32);
   } else {
     // jq-major order: all strings' first jobs, then all second jobs, ...
     // Jobs of one jq have equal size, so static round-robin stays balanced.
@@ -311,6 +317,10 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, Str& st, u3
   st.n_inst = ((st.n + 7) >> 3) / M;
   st.L = st.n_inst ? level_count(st.n_inst) : 1;
   st.J = (u32)job_count(st.n_inst, P.job_lvl);
+  if (VARLEN) {  // merge scratch and counters: multi-job strings only
+    st.scratch = st.J > 1 ? P.meta[2 * s] : 0;
+    st.cnt = st.J > 1 ? P.meta[2 * s + 1] : 0;
+  }
 }
 
 // bytes of job jq (its instances, plus the tail for the last job)

@@ -236,7 +236,11 @@ __global__ void __launch_bounds__(256) plan_tail_kernel(const __grid_constant__ 
         const int cl = jn > 64 ? 64 : (int)jn;
         const u32 pos = atomicAdd(P.cls_cnt + cl, 1u);
         if (pos < P.Q.qb[cl + 1] - P.Q.qb[cl]) {
-          P.queues[P.Q.qb[cl] + pos] = s | (q << 32);
+          u64* rec = P.queues + (P.Q.qb[cl] + pos) * JOB_REC;  // the job's record (decode_job)
+          rec[0] = o0;
+          rec[1] = n;
+          rec[2] = s | (q << 32);
+          rec[3] = 0;
         } else {
           atomicSub(P.cls_cnt + cl, 1u);
           atomicOr(P.err, 2);
@@ -295,7 +299,7 @@ constexpr size_t smem_bytes() {
   constexpr size_t SB = ROUND_INST * M * 8 + 32;
   // ring + mbarriers + parked level-1 group and level-3 accumulator +
   // claimed-job queue (+ per-job EHC seeds in many-seeds mode), per warp
-  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 9 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8 +
+  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 9 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8 * JOB_REC +
                          (PS ? 2 * MAX_EW * 4 : 0)) +
          (NCLS + 1) * 4 + NCLS * 8;  // + varlen class table (per CTA)
 }
@@ -535,7 +539,7 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPl
   p->off_pctl = o; o += 512;  // class counts [NCLS] u32 @0, scratch/counter totals @384
   p->off_clear = o;
   p->off_meta = o; o = align_up(o + n * 16, 256);
-  p->off_queue = o; o = align_up(o + qcap * 8, 256);
+  p->off_queue = o; o = align_up(o + qcap * 8 * JOB_REC, 256);
   p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
   p->off_ztab = o; o = align_up(o + ztab_base(p->lmax + 1, v.k) * 8, 256);
   p->total = o;
@@ -861,6 +865,16 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   return dispatch<true>(output_bytes, P, p.max_jobs, st);
 }
 
+#ifdef HTH_DEBUG_TIMING
+// experiment builds only: copy and clear the per-warp timing records
+int hth_debug_timing(unsigned long long* host, int n_warps) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(host, hth_dbg, (size_t)n_warps * 10 * 8));
+  static unsigned long long zero[8192 * 10];
+  CK(cudaMemcpyToSymbol(hth_dbg, zero, sizeof(zero)));
+  return HTH_OK;
+}
+#endif
 int hth_varlen_status(void* d_workspace, void* stream) {
   if (!d_workspace) return fail(HTH_EINVAL, "null workspace");
   int h = 0;

@@ -13,6 +13,16 @@
 
 namespace hth {
 
+#ifdef HTH_DEBUG_TIMING
+// experiment builds only: per warp {start, end, jobs, rounds, data-wait, valid, claim, decode, rounds, finish} (ns)
+__device__ unsigned long long hth_dbg[8192 * 10];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // Little-endian u64 word `widx` of a stage whose first string byte sits at
 // smem offset `delta` (0..15).  AL: delta % 8 == 0 (aligned LDS.64).
 // Unaligned: three 32-bit shared loads and two funnel shifts (SHF.R.W) for
@@ -261,13 +271,13 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // Jobs are claimed in index order: fixed mode is jq-major (full jobs first),
   // so dynamic claiming also bounds the tail by one job.
   constexpr u32 QN = NS + 4;
-  u64* jq_buf = reinterpret_cast<u64*>(smem + W * NS * SB + W * NS * 8) + W * NACC + warp * QN;
+  u64* jq_buf = reinterpret_cast<u64*>(smem + W * NS * SB + W * NS * 8) + W * NACC + warp * QN * JOB_REC;
   // PS: this warp's EHC seed words for the current job, (lo, hi) pairs
-  u32* ehc_sm = reinterpret_cast<u32*>(jq_buf + (W - warp) * QN) + warp * 2 * MAX_EW;
+  u32* ehc_sm = reinterpret_cast<u32*>(jq_buf + (W - warp) * QN * JOB_REC) + warp * 2 * MAX_EW;
   const EhcSrc<PS> eh{P, ehc_sm};
   // varlen: per size class its first job id (largest class first);
   // cls_pre[0] = total jobs = end of class 1
-  u32* cls_pre = reinterpret_cast<u32*>(smem + W * NS * SB + W * NS * 8 + W * NACC * 8 + W * QN * 8 +
+  u32* cls_pre = reinterpret_cast<u32*>(smem + W * NS * SB + W * NS * 8 + W * NACC * 8 + W * QN * JOB_REC * 8 +
                                         (PS ? W * 2 * MAX_EW * 4 : 0));
   u64 n_jobs = P.n_jobs;
   if (VARLEN) {
@@ -297,7 +307,24 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   u64 psrc = 0;  // next chunk's first byte (global address)
   u64 prem = 0;  // bytes of the current producer job not yet issued
   // cold path: claim the next job and set up its byte range (once per job)
-  auto p_claim = [&]() -> bool {
+#ifdef HTH_DEBUG_TIMING
+  unsigned long long dbg_claim = 0;
+#endif
+  // varlen: job id -> its record in the class queues (one global load)
+  u64 r1[JOB_REC];
+  auto v_fetch = [&](u64 jc) {
+    // the smallest class c with cls_pre[c] <= jc (cls_pre falls as c grows)
+    int lo = 1, hi = NCLS - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cls_pre[mid] <= jc) hi = mid;
+      else lo = mid + 1;
+    }
+    const u64* q = P.job_map + (P.cls_qb[lo] + (jc - cls_pre[lo])) * JOB_REC;
+#pragma unroll
+    for (int i = 0; i < JOB_REC; i++) r1[i] = __ldg(q + i);
+  };
+  auto p_claim_ = [&]() -> bool {
     if (pdone || qhead - qtail >= QN) return false;
     unsigned long long jc = (u64)blockIdx.x * W + warp;
     if (!first) {
@@ -313,28 +340,35 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       pdone = true;
       return false;
     }
-    u64 e = jc;
-    if (VARLEN) {  // job id -> class queue entry
-      // the smallest class c with cls_pre[c] <= jc (cls_pre falls as c grows)
-      int lo = 1, hi = NCLS - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (cls_pre[mid] <= jc) hi = mid;
-        else lo = mid + 1;
+    u64* e = jq_buf + (qhead % QN) * JOB_REC;
+    if constexpr (VARLEN) {
+      v_fetch(jc);
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < JOB_REC; i++) e[i] = r1[i];
       }
-      const int ccur = lo;
-      e = P.job_map[P.cls_qb[ccur] + (jc - cls_pre[ccur])];
+    } else if (lane == 0) {
+      e[0] = jc;
     }
-    if (lane == 0) jq_buf[qhead % QN] = e;
     qhead++;
     Str st;
     u32 jq, ni;
     u64 b0;
-    decode_job<VARLEN, K, M>(P, e, st, jq);
+    decode_job<VARLEN, K, M>(P, jc, r1, st, jq);
     job_span<M>(st, jq, job_lvl, b0, prem, ni);
     psrc = reinterpret_cast<u64>(st.p) + b0;
     return true;
   };
+#ifdef HTH_DEBUG_TIMING
+  auto p_claim = [&]() -> bool {
+    const unsigned long long t = gtimer();
+    const bool r = p_claim_();
+    dbg_claim += gtimer() - t;
+    return r;
+  };
+#else
+  auto& p_claim = p_claim_;
+#endif
   // hot path: one bulk copy per round, address advanced incrementally
   auto p_issue = [&]() {
     while (pseq - cseq < (u32)NS) {
@@ -363,16 +397,24 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   u32 seedL = 0;
   u64 s1A[K], s1B[K];  // level-1 node seeds of this thread's two positions
 #endif
+#ifdef HTH_DEBUG_TIMING
+  unsigned long long dbg_t0 = gtimer(), dbg_jobs = 0, dbg_rounds = 0, dbg_wait = 0, dbg_dec = 0, dbg_loop = 0,
+                     dbg_fin = 0, dbg_m = 0;
+#endif
   for (;;) {
     if (qtail == qhead) p_issue();
     if (qtail == qhead) break;  // no job left anywhere
+#ifdef HTH_DEBUG_TIMING
+    dbg_jobs++;
+    dbg_m = gtimer();
+#endif
     __syncwarp();
-    const u64 job = jq_buf[qtail % QN];
+    const u64* jrec = jq_buf + (qtail % QN) * JOB_REC;
     qtail++;
     Str st;
     u32 jq, ninst;
     u64 byte0, nbytes;
-    decode_job<VARLEN, K, M>(P, job, st, jq);
+    decode_job<VARLEN, K, M>(P, jrec[0], jrec, st, jq);
     job_span<M>(st, jq, job_lvl, byte0, nbytes, ninst);
     const u32 nchunks = (u32)ceil_div(nbytes, CB);
     const u32 delta = (u32)(reinterpret_cast<uintptr_t>(st.p) & 15);
@@ -399,6 +441,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     }
 #endif
 
+#ifdef HTH_DEBUG_TIMING
+    { const unsigned long long t = gtimer(); dbg_dec += t - dbg_m; dbg_m = t; }
+#endif
     u64 fin[K];
     u32 events = last_job ? 1u : 0u;
 #pragma unroll
@@ -420,7 +465,14 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       constexpr bool FULL = decltype(full_c)::value;
       for (u32 c = 0; c < nchunks; c++) {
         const u32 slot = cseq % NS;
+#ifdef HTH_DEBUG_TIMING
+        const unsigned long long dbg_w = gtimer();
         mbar_wait(&bars[slot], (cseq / NS) & 1);
+        dbg_wait += gtimer() - dbg_w;
+        dbg_rounds++;
+#else
+        mbar_wait(&bars[slot], (cseq / NS) & 1);
+#endif
         uint8_t* buf = ring + slot * SB;
         const bool tail_chunk = !FULL && last_job && (c + 1 == nchunks);
         if (tail_chunk && (st.n & 7)) {
@@ -545,6 +597,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     else
       rounds(std::false_type{});
 
+#ifdef HTH_DEBUG_TIMING
+    { const unsigned long long t = gtimer(); dbg_loop += t - dbg_m; dbg_m = t; }
+#endif
     if (last_job && P.fin_const_ok) {
       if (lane == 0) {
 #pragma unroll
@@ -608,7 +663,20 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
         if (lane == 0) P.events[st.s] = 0;
       }
     }
+#ifdef HTH_DEBUG_TIMING
+    dbg_fin += gtimer() - dbg_m;
+#endif
   }
+#ifdef HTH_DEBUG_TIMING
+  if (lane == 0) {
+    const u64 gw = (u64)blockIdx.x * W + warp;
+    if (gw < 8192) {
+      unsigned long long* d = hth_dbg + gw * 10;
+      d[0] = dbg_t0; d[1] = gtimer(); d[2] = dbg_jobs; d[3] = dbg_rounds; d[4] = dbg_wait; d[5] = 1;
+      d[6] = dbg_claim; d[7] = dbg_dec; d[8] = dbg_loop; d[9] = dbg_fin;
+    }
+  }
+#endif
   // every warp has stopped claiming; the last one out re-zeroes the counters
   // (relaxed is enough: each warp's last claim returned before it got here)
   if (claims && lane == 0) {
