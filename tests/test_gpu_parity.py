@@ -470,6 +470,39 @@ def test_varlen_bound_violation_is_flagged(hh):
     assert rc == 0 and L.hth_varlen_status(ws.data_ptr(), st) == 0
 
 
+def test_varlen_undeclared_bytes_are_flagged(hh):
+    # total_bytes sizes the job queues; a batch holding more instances than it
+    # declares must be reported (HTH_EINVAL), never written out of bounds
+    import torch
+
+    from paper_2104_08865_b200 import _lib, batch
+
+    p = hh.variant(40)
+    lengths = np.full(300, 960 * 3, dtype=np.uint64)  # 300 strings of 3 instances
+    off = np.zeros(301, dtype=np.uint64)
+    off[1:] = np.cumsum(lengths)
+    total = int(off[-1])
+    buf = hh.fill_bytes(total, 4)
+    seed = hh.seed_for_input(b"\1" * 32, p, 960 * 3)
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    out = torch.empty((300, 5), dtype=torch.int64, device="cuda")
+    small = 960 * 3 * 10  # declares 10 strings' worth
+    ws = torch.zeros(batch.workspace_varlen(p, 300, small) + 4096, dtype=torch.uint8, device="cuda")
+    guard = ws[-4096:].clone()
+    st = torch.cuda.current_stream().cuda_stream
+    L = _lib.lib()
+    rc = L.hth_hash_varlen(40, buf.data_ptr(), d_off.data_ptr(), 300, 960 * 3, small, seed.fold,
+                           seed.device_words().data_ptr(), seed.capacity, out.data_ptr(), ws.data_ptr(),
+                           ws.numel() - 4096, st)
+    assert rc == 0
+    assert L.hth_varlen_status(ws.data_ptr(), st) == _lib.HTH_EINVAL
+    assert torch.equal(ws[-4096:], guard)  # nothing written past the declared workspace
+    # declared correctly, the same batch hashes cleanly and matches the oracle
+    got = _u64(hh.hash_varlen(buf, off, seed, p))
+    host = np.frombuffer(o.fill_bytes(total, 4), dtype=np.uint8).copy()
+    assert np.array_equal(got, coracle.hash_varlen(40, host, off, seed.words_np(0, seed.capacity)))
+
+
 def test_concurrent_streams(hh):
     # independent calls on two streams with their own workspaces give the same digests
     import torch
