@@ -93,21 +93,13 @@ __device__ __forceinline__ u64 nh_acc(u64 acc, w2 x, u32 slo, u32 shi) { return 
 __device__ __forceinline__ u64 nh_acc(u64 acc, w2 x, u64 s) { return nh_acc(acc, x, (u32)s, (u32)(s >> 32)); }
 __device__ __forceinline__ u64 nh_acc(u64 acc, u64 x, u64 s) { return nh_acc(acc, mk(x), s); }
 
-// acc += C * h (mod 2^64) for a small constant C in two IMADs: the low half
-// as one IMAD.WIDE.U32 (carry included), the high half as one IMAD.
+// acc += C * h (mod 2^64) for a small constant C.  Written as plain C++ so
+// ptxas picks LEA + LEA.HI.X for powers of two and IMAD.WIDE.U32 (with the
+// accumulator) + IMAD + IADD3 otherwise; an inline-PTX mad.wide/mad.lo pair
+// was split by ptxas into four instructions per term.
 template <int C>
 __device__ __forceinline__ u64 mac_const(u64 acc, u64 h) {
-  if (C == 0) return acc;
-  u64 r;
-  asm("{\n .reg .u32 lo, hi, hl, hh;\n"
-      " mov.b64 {hl, hh}, %2;\n"
-      " mad.wide.u32 %0, hl, %3, %1;\n"
-      " mov.b64 {lo, hi}, %0;\n"
-      " mad.lo.u32 hi, hh, %3, hi;\n"
-      " mov.b64 %0, {lo, hi};\n}"
-      : "=l"(r)
-      : "l"(acc), "l"(h), "n"(C));
-  return r;
+  return acc + h * (u64)C;
 }
 
 // x * v on 16 bit-sliced GF(16) elements (gf16.py:17-21), in 32-bit halves:
@@ -271,11 +263,15 @@ struct Params {
   u64* frontier;
   // EHC seed words S[0..e*w), split into halves.  The kernel takes Params as
   // a __grid_constant__, so these are constant-bank operands of the NH adds.
-  // Interleaved (lo, hi) so one 64-bit constant load fetches both halves.
-  alignas(8) u32 ehc[2 * MAX_EW];
+  // Interleaved (lo, hi), word i at slot ehc_slot(i): the leaf's block-u pass
+  // reads its e words from consecutive slots (16-byte constant loads).
+  alignas(16) u32 ehc[2 * MAX_EW];
   // varlen: start of each size class's queue in job_map (host-computed; [NCLS] = end)
   u64 cls_qb[NCLS + 1];
 };
+
+// slot of EHC seed word idx = item * w + u in Params::ehc: u-major
+__host__ __device__ constexpr int ehc_slot(int idx, int e, int w) { return (idx % w) * e + idx / w; }
 
 template <int K>
 __device__ __forceinline__ void layout_bases(u32 L, int ew, u64 (&T)[K], u64 (&F)[K], u64& R) {

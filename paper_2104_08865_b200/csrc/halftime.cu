@@ -76,8 +76,9 @@ u64 host_mix(u64 z) {
 void fill_ehc(const VarInfo& v, u64 fold, Params& P) {
   for (int i = 0; i < v.ew; i++) {
     const u64 w = host_mix(fold + (u64)(i + 1) * 0x9E3779B97F4A7C15ull);
-    P.ehc[2 * i] = (u32)w;
-    P.ehc[2 * i + 1] = (u32)(w >> 32);
+    const int slot = ehc_slot(i, v.e, v.w);
+    P.ehc[2 * slot] = (u32)w;
+    P.ehc[2 * slot + 1] = (u32)(w >> 32);
   }
 }
 

@@ -66,12 +66,17 @@ __device__ __forceinline__ u64 mac_coef(int c, u64 acc, u64 h) {
 
 // EHC seed words: constant-bank kernel parameters (one seed for the launch)
 // or, PERSEED, the job's words staged in shared memory.
-template <bool PERSEED>
+template <bool PERSEED, int OUT>
 struct EhcSrc {
   const Params& P;
   const u32* sm;
-  __device__ __forceinline__ u32 lo(int i) const { return PERSEED ? sm[2 * i] : P.ehc[2 * i]; }
-  __device__ __forceinline__ u32 hi(int i) const { return PERSEED ? sm[2 * i + 1] : P.ehc[2 * i + 1]; }
+  static constexpr int E = Var<OUT>::e, WB = Var<OUT>::w;
+  __device__ __forceinline__ u32 lo(int i) const {
+    return PERSEED ? sm[2 * ehc_slot(i, E, WB)] : P.ehc[2 * ehc_slot(i, E, WB)];
+  }
+  __device__ __forceinline__ u32 hi(int i) const {
+    return PERSEED ? sm[2 * ehc_slot(i, E, WB) + 1] : P.ehc[2 * ehc_slot(i, E, WB) + 1];
+  }
 };
 
 // EHC leaf of two instances, lane j -> CA[r], CB[r] (hasher.py:356-364;
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   u64* jq_buf = reinterpret_cast<u64*>(smem + W * NS * SB + W * NS * 8) + W * NACC + warp * QN * JOB_REC;
   // PS: this warp's EHC seed words for the current job, (lo, hi) pairs
   u32* ehc_sm = reinterpret_cast<u32*>(jq_buf + (W - warp) * QN * JOB_REC) + warp * 2 * MAX_EW;
-  const EhcSrc<PS> eh{P, ehc_sm};
+  const EhcSrc<PS, OUT> eh{P, ehc_sm};
   // varlen: per size class its first job id (largest class first);
   // cls_pre[0] = total jobs = end of class 1
   u32* cls_pre = reinterpret_cast<u32*>(smem + W * NS * SB + W * NS * 8 + W * NACC * 8 + W * QN * JOB_REC * 8 +
@@ -425,8 +430,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       __syncwarp();
       if (lane < Geo<V>::ew) {
         const u64 w = splitmix_word(st.fold, lane);
-        ehc_sm[2 * lane] = (u32)w;
-        ehc_sm[2 * lane + 1] = (u32)(w >> 32);
+        const int slot = ehc_slot(lane, Var<OUT>::e, Var<OUT>::w);
+        ehc_sm[2 * slot] = (u32)w;
+        ehc_sm[2 * slot + 1] = (u32)(w >> 32);
       }
       __syncwarp();
     }

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(W * 32, MINB) small_kernel(const __grid_consta
   TreeCtx<K, Geo<V>::ew> tc;
   tc.L = 1;  // n_inst < 8: a single level (hasher.py:130-153)
   const SeedSrc<false> sd{P.S, 0};
-  const EhcSrc<false> eh{P, nullptr};
+  const EhcSrc<false, OUT> eh{P, nullptr};
   const u64 units = (P.n_strings + G - 1) / G;
   const u64 NW = (u64)gridDim.x * W;
   const u64 w0 = (u64)blockIdx.x * W + warp;
