@@ -228,6 +228,8 @@ struct Params {
   u64 stride;    // fixed mode
   u64 n_bytes;   // fixed mode: length; varlen: length clamp (host-checked bound)
   u64 J_fixed;   // fixed mode: jobs per string
+  u64 n_inst_fixed;  // fixed mode: instances per string
+  u32 L_fixed;       // fixed mode: layout levels per string
   u64 n_jobs;    // fixed mode: total jobs
   u64 scr_per;   // fixed mode: scratch words per string
   u64 cnt_per;   // fixed mode: counters per string
@@ -310,9 +312,15 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, const u64* 
   if (!VARLEN && P.frontier_lvl) {  // slice mode: P.n_bytes is the whole string
     jq += (u32)P.slice_job0;
   }
-  st.n_inst = ((st.n + 7) >> 3) / M;
-  st.L = st.n_inst ? level_count(st.n_inst) : 1;
-  st.J = (u32)job_count(st.n_inst, P.job_lvl);
+  if (VARLEN) {
+    st.n_inst = ((st.n + 7) >> 3) / M;
+    st.L = st.n_inst ? level_count(st.n_inst) : 1;
+    st.J = (u32)job_count(st.n_inst, P.job_lvl);
+  } else {  // launch constants (kept out of the per-round producer path)
+    st.n_inst = P.n_inst_fixed;
+    st.L = P.L_fixed;
+    st.J = (u32)P.J_fixed;
+  }
   if (VARLEN) {  // merge scratch and counters: multi-job strings only
     st.scratch = st.J > 1 ? P.meta[2 * s] : 0;
     st.cnt = st.J > 1 ? P.meta[2 * s + 1] : 0;

@@ -698,6 +698,8 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.stride = stride_bytes;
   P.n_bytes = n_bytes;
   P.J_fixed = f.J;
+  P.n_inst_fixed = f.n_inst;
+  P.L_fixed = f.n_inst ? level_count(f.n_inst) : 1;
   P.n_jobs = f.n_jobs;
   P.scr_per = f.scr_per;
   P.cnt_per = f.cnt_per;
@@ -765,6 +767,8 @@ int hth_hash_fixed_folds(int output_bytes, const void* d_data, uint64_t n_string
   P.stride = stride_bytes;
   P.n_bytes = n_bytes;
   P.J_fixed = f.J;
+  P.n_inst_fixed = f.n_inst;
+  P.L_fixed = f.n_inst ? level_count(f.n_inst) : 1;
   P.n_jobs = f.n_jobs;
   P.scr_per = f.scr_per;
   P.cnt_per = f.cnt_per;
@@ -942,6 +946,8 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   P.stride = 0;
   P.n_bytes = n_bytes;
   P.J_fixed = f.J;
+  P.n_inst_fixed = f.n_inst;
+  P.L_fixed = f.n_inst ? level_count(f.n_inst) : 1;
   P.n_jobs = j1 - j0;
   P.S = d_seed;
   P.out = d_partial;

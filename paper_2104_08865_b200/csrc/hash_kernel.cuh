@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   bool first = HTH_STATIC_FIRST || !claims;
   u32 pseq = 0, cseq = 0;
   u64 psrc = 0;  // next chunk's first byte (global address)
-  u64 prem = 0;  // bytes of the current producer job not yet issued
+  u32 prem = 0;  // bytes of the current producer job not yet issued (a job is < 4 GiB)
   // cold path: claim the next job and set up its byte range (once per job)
 #ifdef HTH_DEBUG_TIMING
   unsigned long long dbg_claim = 0;
@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     u32 jq, ni;
     u64 b0;
     decode_job<VARLEN, K, M>(P, jc, r1, st, jq);
-    job_span<M>(st, jq, job_lvl, b0, prem, ni);
+    u64 jbytes;
+    job_span<M>(st, jq, job_lvl, b0, jbytes, ni);
+    prem = (u32)jbytes;
     psrc = reinterpret_cast<u64>(st.p) + b0;
     return true;
   };
@@ -375,23 +377,26 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   auto& p_claim = p_claim_;
 #endif
   // hot path: one bulk copy per round, address advanced incrementally
+  auto p_issue_one = [&]() {
+    const u32 len = min(CB, prem);
+    const u64 a0 = psrc & ~15ull;
+    const u32 bytes = (u32)(((psrc + len + 15) & ~15ull) - a0);
+    const u32 slot = pseq % NS;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[slot], bytes);
+      bulk_g2s(ring + slot * SB, reinterpret_cast<const void*>(a0), bytes, &bars[slot], pol);
+    }
+    pseq++;
+    psrc += CB;
+    prem -= len;
+  };
   auto p_issue = [&]() {
     while (pseq - cseq < (u32)NS) {
       if (prem == 0) {
         if (!p_claim()) return;
         continue;
       }
-      const u32 len = (u32)min((u64)CB, prem);
-      const u64 a0 = psrc & ~15ull;
-      const u32 bytes = (u32)(((psrc + len + 15) & ~15ull) - a0);
-      const u32 slot = pseq % NS;
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&bars[slot], bytes);
-        bulk_g2s(ring + slot * SB, reinterpret_cast<const void*>(a0), bytes, &bars[slot], pol);
-      }
-      pseq++;
-      psrc += CB;
-      prem -= len;
+      p_issue_one();
     }
   };
   p_issue();
@@ -595,7 +600,11 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
         }
         __syncwarp();
         cseq++;
-        p_issue();
+        // the ring was full (or the producer is out of bytes): refill one slot
+        if (prem != 0 && pseq - cseq == (u32)NS - 1)
+          p_issue_one();
+        else
+          p_issue();
       }
     };
     if (!VARLEN && !last_job && ninst == (1u << (3 * job_lvl)))
