@@ -15,7 +15,8 @@ if wk.startswith("fixed:"):  # fixed:<variant>:<n_strings>:<n_bytes>
     bench.wl.CONFIGS[wk] = dict(desc=wk, variant=int(w_), n_strings=int(b_), n_bytes=int(n_))
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 ctx = bench.setup_fixed(hh, torch, wk)
-total_ms, per, _ = bench.run_fixed(hh, torch, ctx, steps, 5)
+flush = bench.make_flush(torch) if wk == "cfg1" else None  # as bench.py: L2 flushed per step
+total_ms, per, _ = bench.run_fixed(hh, torch, ctx, steps, 5, flush)
 ms = total_ms / steps
 gbs = ctx["B"] * ctx["n"] / ms / 1e6
 from oracle import c as coracle  # noqa: E402
