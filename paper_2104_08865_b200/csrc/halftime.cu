@@ -548,6 +548,10 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPl
 }
 
 // per-thread e2e context (device buffers reused across calls)
+// host calls up to this many input bytes (and digest words) take the
+// one-stream path through pinned staging: a single-string hash_bytes call is
+// then one H2D DMA, one launch, one D2H DMA and one synchronize
+constexpr u64 kSmallCall = 256 << 10, kSmallOut = 4096;
 struct HostCtx {
   int dev = -1;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
@@ -559,6 +563,11 @@ struct HostCtx {
   u64 out_words = 0;
   void* ws[3] = {nullptr, nullptr, nullptr};
   u64 ws_bytes = 0;
+  // small-call path: pinned staging both ways, and the fold whose first
+  // `seeds_valid` words are already expanded in `seeds`
+  uint8_t* hin = nullptr;
+  u64* hout = nullptr;
+  u64 seeds_fold = 0, seeds_valid = 0;
   ~HostCtx() {}
 };
 thread_local HostCtx g_host;
@@ -582,6 +591,7 @@ int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_by
     if (c.seeds) cudaFree(c.seeds);
     CK(cudaMalloc(&c.seeds, seed_words * 8));
     c.seed_words = seed_words;
+    c.seeds_valid = 0;
   }
   if (out_words > c.out_words) {
     if (c.out) cudaFree(c.out);
@@ -598,7 +608,23 @@ int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_by
     CK(cudaDeviceSynchronize());
     c.ws_bytes = ws_bytes;
   }
+  if (!c.hin) {
+    CK(cudaHostAlloc((void**)&c.hin, kSmallCall + 16, cudaHostAllocDefault));
+    CK(cudaHostAlloc((void**)&c.hout, kSmallOut * 8, cudaHostAllocDefault));
+  }
   *out = &c;
+  return HTH_OK;
+}
+
+}  // namespace
+extern "C" int hth_expand_seed(uint64_t fold, uint64_t start, uint64_t count, uint64_t* d_words, void* stream);
+namespace {
+// seed words [0, total) of `fold` in c.seeds, expanded on st unless already there
+int host_seeds(HostCtx* c, u64 fold, u64 total, cudaStream_t st) {
+  if (c->seeds_valid >= total && c->seeds_fold == fold) return HTH_OK;
+  if (int rc = hth_expand_seed(fold, 0, total, c->seeds, st)) return rc;
+  c->seeds_fold = fold;
+  c->seeds_valid = total;
   return HTH_OK;
 }
 
@@ -1032,7 +1058,24 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
   HostCtx* c = nullptr;
   if (int rc = host_ctx(device, per * dstride + 16, lay.total, n_strings * v.k, std::max<u64>(fp.ws_total, 256), &c))
     return rc;
-  if (int rc = hth_expand_seed(fold_of(master), 0, lay.total, c->seeds, c->st[0])) return rc;
+  const u64 fold = fold_of(master);
+  const u64 in_bytes = n_bytes ? (n_strings - 1) * stride_bytes + n_bytes : 0;
+  if (nchunks == 1 && in_bytes <= kSmallCall && n_strings * v.k <= kSmallOut) {
+    cudaStream_t st = c->st[0];
+    if (int rc = host_seeds(c, fold, lay.total, st)) return rc;
+    if (in_bytes) {
+      std::memcpy(c->hin, h_data, in_bytes);
+      CK(cudaMemcpyAsync(c->buf[0], c->hin, in_bytes, cudaMemcpyHostToDevice, st));
+    }
+    if (int rc = hth_hash_fixed(output_bytes, c->buf[0], n_strings, dstride, n_bytes, fold, c->seeds, lay.total,
+                                c->out, c->ws[0], c->ws_bytes, st))
+      return rc;
+    CK(cudaMemcpyAsync(c->hout, c->out, n_strings * v.k * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(h_out, c->hout, n_strings * v.k * 8);
+    return HTH_OK;
+  }
+  if (int rc = host_seeds(c, fold, lay.total, c->st[0])) return rc;
   cudaEvent_t seeded;
   CK(cudaEventCreateWithFlags(&seeded, cudaEventDisableTiming));
   CK(cudaEventRecord(seeded, c->st[0]));
