@@ -455,12 +455,19 @@ def arm_ours(args, rank, world, local_rank):
 
     import paper_2104_08865_b200 as hh
 
+    local_rank %= max(torch.cuda.device_count(), 1)  # HTH_BENCH_BACKEND=gloo runs share one GPU
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # HTH_BENCH_BACKEND=gloo: exercise the multi-rank code path with several
+        # ranks on one GPU (no kernel waits on another rank; timing not meaningful)
+        backend = os.environ.get("HTH_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     peak, peak_src = _peaks()
     workload = args.workload
     ctx = setup_fixed(hh, torch, workload, rank, world)
