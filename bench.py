@@ -453,8 +453,11 @@ def arm_reference(args, rank, world):
 def arm_split(args, rank, world, local_rank, hh, torch, dist):
     """Config 5 on N > 1 GPUs: ONE 16 GiB string split at multiples of 8^c
     instances (hth_slice_plan); each rank generates and hashes its slice in
-    place (hth_hash_slice), the level-c subtree roots and partial digests are
-    gathered to rank 0 (all_gather) which finishes the tree (hth_hash_merge).
+    place (hth_hash_slice), the level-c subtree roots and partial digests go
+    to rank 0 -- stored by the slice kernels straight into rank 0's memory
+    through CUDA-IPC peer pointers (--exchange p2p, default; one barrier) or
+    moved by all_gather (--exchange nccl) -- and rank 0 finishes the tree
+    (hth_hash_merge).
     A step = the whole string: slice kernel + exchange + merge; total work is
     fixed as N grows (strong scaling)."""
     from paper_2104_08865_b200 import multi_gpu
@@ -475,7 +478,10 @@ def arm_split(args, rank, world, local_rank, hh, torch, dist):
     def step():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        d = multi_gpu.hash_string_distributed(buf, plan, seed)
+        if args.exchange == "p2p":
+            d = multi_gpu.hash_string_p2p(buf, plan, seed)
+        else:
+            d = multi_gpu.hash_string_distributed(buf, plan, seed)
         b.record(stream)
         kern.append((a, b))
         return d
@@ -520,7 +526,9 @@ def arm_split(args, rank, world, local_rank, hh, torch, dist):
                        "sharding": f"one string split at multiples of 8^{plan.level} instances",
                        "slices_instances": list(plan.bounds), "frontier_roots": plan.n_frontier,
                        "l2": "inputs larger than L2 (126 MB); no flush needed",
-                       "parallelism": f"dp{world} slices + all_gather of subtree roots + merge on rank 0"},
+                       "exchange": ("slice kernels store roots/partials into rank 0's memory (CUDA IPC, NVLink) + barrier"
+                                    if args.exchange == "p2p" else "all_gather of roots/partials"),
+                       "parallelism": f"dp{world} slices + root exchange + merge on rank 0"},
             "roofline": {"bound": "hbm", "achieved": (b1 - b0) / (step_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": (b1 - b0) / (step_ms / 1e3) / 1e9 / peak, "traffic": None,
                          "kernel": "rank 0 step: hash_kernel<16> slice + all_gather + merge_kernel",
@@ -666,6 +674,8 @@ def main():
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-strings", type=int, default=0, help="cap e2e batch (0 = full config)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="cfg5 on N > 1 GPUs: how the subtree roots reach rank 0")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

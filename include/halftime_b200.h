@@ -148,6 +148,17 @@ int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const
                    uint64_t n_frontier, const uint64_t* d_partials, uint64_t n_partials, uint64_t seed_fold,
                    const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out, void* d_workspace,
                    uint64_t workspace_bytes, void* stream);
+/* Peer-memory exchange for the split string (no reference counterpart: the
+ * reference is single-process).  Rank 0 exports its gather buffer
+ * (hth_ipc_get_handle: 64 opaque bytes naming the enclosing allocation, plus
+ * the buffer's byte offset inside it, sent to the other ranks); each rank
+ * maps it (hth_ipc_open_handle, peer access over NVLink), adds the offset and
+ * passes pointers into it as hth_hash_slice's d_frontier / d_partial, so the
+ * slice kernel itself stores its subtree roots and partial digest into rank
+ * 0's memory.  hth_ipc_close_handle unmaps (the mapped base). */
+int hth_ipc_get_handle(const void* d_ptr, uint8_t handle_out[64], uint64_t* offset_out);
+int hth_ipc_open_handle(const uint8_t handle[64], void** d_ptr_out);
+int hth_ipc_close_handle(void* d_ptr);
 
 /* ---- host-buffer entry points (end-to-end; synchronous).  These are what
  * hash_bytes(..., engine="cuda") binds: host bytes in, host digest words

@@ -24,6 +24,7 @@ EXPORTS = (
     "hth_workspace_size_fixed", "hth_hash_fixed", "hth_workspace_size_varlen",
     "hth_hash_varlen", "hth_varlen_status", "hth_hash_host", "hth_hash_fixed_host",
     "hth_slice_plan", "hth_workspace_size_slice", "hth_hash_slice", "hth_hash_merge", "hth_hash_fixed_folds",
+    "hth_ipc_get_handle", "hth_ipc_open_handle", "hth_ipc_close_handle",
 )
 
 _lock = threading.Lock()
@@ -67,6 +68,9 @@ def lib() -> ctypes.CDLL:
             "hth_workspace_size_slice": [i32, u64, pu64],
             "hth_hash_slice": [i32, vp, u64, u64, u64, i32, u64, vp, u64, vp, vp, vp, u64, vp],
             "hth_hash_merge": [i32, u64, i32, vp, u64, vp, u64, u64, vp, u64, vp, vp, u64, vp],
+            "hth_ipc_get_handle": [vp, vp, pu64],
+            "hth_ipc_open_handle": [vp, ctypes.POINTER(ctypes.c_void_p)],
+            "hth_ipc_close_handle": [vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)

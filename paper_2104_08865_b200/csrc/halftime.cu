@@ -944,6 +944,44 @@ int hth_workspace_size_slice(int output_bytes, uint64_t n_bytes, uint64_t* bytes
   return hth_workspace_size_fixed(output_bytes, 1, n_bytes, bytes);
 }
 
+int hth_ipc_get_handle(const void* d_ptr, uint8_t handle_out[64], uint64_t* offset_out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (!d_ptr || !handle_out || !offset_out) return fail(HTH_EINVAL, "null pointer");
+  // the handle names the whole allocation (e.g. a caching-allocator segment):
+  // report where d_ptr sits inside it
+  typedef int (*AddrRange)(unsigned long long*, size_t*, unsigned long long);
+  static AddrRange range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) return fail(HTH_ECUDA, "cuMemGetAddressRange unavailable");
+    range = (AddrRange)fn;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)(uintptr_t)d_ptr) != 0) return fail(HTH_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+  std::memcpy(handle_out, &h, 64);
+  *offset_out = (uint64_t)((uintptr_t)d_ptr - base);
+  return HTH_OK;
+}
+
+int hth_ipc_open_handle(const uint8_t handle[64], void** d_ptr_out) {
+  if (!handle || !d_ptr_out) return fail(HTH_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  CK(cudaIpcOpenMemHandle(d_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return HTH_OK;
+}
+
+int hth_ipc_close_handle(void* d_ptr) {
+  if (!d_ptr) return fail(HTH_EINVAL, "null pointer");
+  CK(cudaIpcCloseMemHandle(d_ptr));
+  return HTH_OK;
+}
+
 int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
                    int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
                    uint64_t* d_frontier, uint64_t* d_partial, void* d_workspace, uint64_t workspace_bytes,

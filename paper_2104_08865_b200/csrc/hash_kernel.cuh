@@ -692,6 +692,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     }
   }
 #endif
+  // slice mode: the frontier roots and partial digest may live in another
+  // GPU's memory (peer stores over NVLink); make them visible system-wide
+  if (P.frontier_lvl) __threadfence_system();
   // every warp has stopped claiming; the last one out re-zeroes the counters
   // (relaxed is enough: each warp's last claim returned before it got here)
   if (claims && lane == 0) {

@@ -8,7 +8,10 @@
   subtree roots; finalize terms (tree.py:103-134) and the Toeplitz tail
   (hasher.py:186-206) are sums, so each slice also yields a partial digest.
   The only exchange is gathering the roots (<= a few hundred KB) and the
-  partials to rank 0, which finishes the tree with ``hth_hash_merge``.
+  partials to rank 0, which finishes the tree with ``hth_hash_merge``:
+  either the slice kernels store them straight into rank 0's memory over
+  NVLink (``hash_string_p2p``: peer pointers from CUDA IPC, one barrier per
+  string) or an NCCL ``all_gather`` moves them (``hash_string_distributed``).
 """
 
 from __future__ import annotations
@@ -159,4 +162,106 @@ def hash_string_distributed(local, plan: SlicePlan, seed: SeedBuffer, group=None
         return None
     frontier = torch.cat([frs[i][:plan.counts[i]] for i in range(world)], dim=0)
     digest = merge_fn(frontier, torch.stack(parts), plan, seed)
+    return digest.cpu().numpy().view(np.uint64).copy()
+
+
+# ------------------------------------------------------------------ peer-memory exchange
+_P2P = {}
+
+
+def _ipc_handle(ptr: int):
+    """(64-byte handle of the allocation holding ptr, ptr's offset in it)"""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64()
+    _lib.check(_lib.lib().hth_ipc_get_handle(ptr, h, ctypes.byref(off)))
+    return h.raw, int(off.value)
+
+
+_IPC_OPEN = {}  # allocation handle -> mapped base (a process maps each allocation once)
+
+
+def _ipc_open(handle) -> int:
+    raw, off = handle
+    base = _IPC_OPEN.get(raw)
+    if base is None:
+        buf = ctypes.create_string_buffer(raw, 64)
+        out = ctypes.c_void_p()
+        _lib.check(_lib.lib().hth_ipc_open_handle(buf, ctypes.byref(out)))
+        base = _IPC_OPEN[raw] = int(out.value)
+    return base + off
+
+
+def _p2p_buffers(plan: SlicePlan, dev, group):
+    """Rank 0's two gather buffers (double-buffered across calls), mapped into
+    every rank: [frontier roots of all slices in slice order | one partial
+    digest per slice].  Returns (local tensors or None, base addresses)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    key = (plan, dev.index, id(group))
+    ent = _P2P.get(key)
+    if ent is not None:
+        return ent
+    k = plan.params.output_words
+    words = plan.n_frontier * 8 * k + plan.n_slices * k
+    buf, handle = None, None
+    if rank == 0:
+        # both slots in one tensor: one IPC handle (a process maps a handle once)
+        buf = torch.zeros(2 * max(words, 1), dtype=torch.int64, device=dev)
+        handle = _ipc_handle(buf.data_ptr())
+    obj = [handle]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    b0 = buf.data_ptr() if rank == 0 else _ipc_open(obj[0])
+    bases = [b0, b0 + 8 * max(words, 1)]
+    bufs = [buf[:max(words, 1)], buf[max(words, 1):]] if rank == 0 else None
+    ent = {"bufs": bufs, "bases": bases, "words": words, "step": 0}
+    _P2P[key] = ent
+    return ent
+
+
+def hash_string_p2p(local, plan: SlicePlan, seed: SeedBuffer, group=None):
+    """Like ``hash_string_distributed`` but without a collective on the data
+    path: slice i's kernel (hth_hash_slice) writes its subtree roots and its
+    partial digest directly into rank 0's gather buffer through a CUDA-IPC
+    peer mapping (NVLink stores), then one barrier; rank 0 merges.  Rank 0
+    returns the (k,) digest words (numpy uint64), other ranks None.  The two
+    gather buffers alternate, so a rank may start the next string while rank 0
+    still merges this one."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    if world != plan.n_slices:
+        raise ValueError("plan must have one slice per rank")
+    p = plan.params
+    _check_capacity(seed, p, plan.n_bytes)
+    k = p.output_words
+    dev = local.device
+    ent = _p2p_buffers(plan, dev, group)
+    slot = ent["step"] & 1
+    ent["step"] += 1
+    base = ent["bases"][slot]
+    nfw = plan.n_frontier * 8 * k
+    fr_ptr = base + sum(plan.counts[:rank]) * 8 * k * 8
+    part_ptr = base + (nfw + rank * k) * 8
+    wsz = ctypes.c_uint64()
+    _lib.check(_lib.lib().hth_workspace_size_slice(p.output_bytes, plan.n_bytes, ctypes.byref(wsz)))
+    ws = _ws(dev, wsz.value)
+    b0, b1 = plan.byte_range(rank)
+    if local.numel() < b1 - b0:
+        raise ValueError("slice tensor shorter than its byte range")
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        _lib.check(_lib.lib().hth_hash_slice(
+            p.output_bytes, local.data_ptr(), plan.n_bytes, plan.bounds[rank], plan.bounds[rank + 1], plan.level,
+            seed.fold, seed.device_words(dev).data_ptr(), seed.capacity, fr_ptr, part_ptr, ws.data_ptr(),
+            ws.numel(), stream.cuda_stream))
+        stream.synchronize()  # this slice's roots and partial are in rank 0's memory
+    dist.barrier(group=group)
+    if rank != 0:
+        return None
+    g = ent["bufs"][slot]
+    digest = hash_merge(g[:nfw].view(plan.n_frontier, 8 * k), g[nfw:nfw + world * k].view(world, k), plan, seed)
     return digest.cpu().numpy().view(np.uint64).copy()
