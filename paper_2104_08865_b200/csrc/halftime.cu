@@ -5,6 +5,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <omp.h>
 #include <tuple>
 #include <string>
 #include <vector>
@@ -568,6 +570,9 @@ struct HostCtx {
   uint8_t* hin = nullptr;
   u64* hout = nullptr;
   u64 seeds_fold = 0, seeds_valid = 0;
+  // pageable sources: two pinned staging slots filled by parallel memcpy
+  uint8_t* ring[2] = {nullptr, nullptr};
+  cudaEvent_t ring_ev[2] = {nullptr, nullptr};
   ~HostCtx() {}
 };
 thread_local HostCtx g_host;
@@ -619,6 +624,48 @@ int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_by
 }  // namespace
 extern "C" int hth_expand_seed(uint64_t fold, uint64_t start, uint64_t count, uint64_t* d_words, void* stream);
 namespace {
+constexpr u64 kRing = 16ull << 20;  // bytes per pinned staging slot
+
+// memcpy with several host threads (one thread reaches ~10 GB/s; the PCIe
+// link takes ~55).  num_threads overrides OMP_NUM_THREADS=1 set by launchers.
+void par_memcpy(void* dst, const void* src, u64 n) {
+  const int T = (int)std::min<unsigned>(32, std::max(1u, std::thread::hardware_concurrency()));
+#pragma omp parallel for num_threads(T) schedule(static)
+  for (int t = 0; t < T; t++) {
+    const u64 lo = (n * t / T) & ~63ull, hi = t + 1 == T ? n : (n * (t + 1) / T) & ~63ull;
+    if (hi > lo) std::memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
+  }
+}
+
+// host -> device copy on st.  Pinned sources (and small copies) go straight to
+// the DMA engine; large pageable ones through the pinned staging slots:
+// parallel memcpy of slice i+1 overlaps the DMA of slice i.
+int h2d(HostCtx* c, void* dst, const void* src, u64 bytes, cudaStream_t st) {
+  cudaPointerAttributes a{};
+  const bool pinned = cudaPointerGetAttributes(&a, src) == cudaSuccess && a.type != cudaMemoryTypeUnregistered;
+  cudaGetLastError();  // clear a sticky error from the attribute query on plain pointers
+  if (pinned || bytes < (8ull << 20)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return HTH_OK;
+  }
+  for (int i = 0; i < 2; i++) {
+    if (!c->ring[i]) {
+      CK(cudaHostAlloc((void**)&c->ring[i], kRing, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
+    }
+  }
+  u64 i = 0;
+  for (u64 off = 0; off < bytes; off += kRing, i++) {
+    const int slot = (int)(i & 1);
+    const u64 len = std::min(kRing, bytes - off);
+    CK(cudaEventSynchronize(c->ring_ev[slot]));  // the slot's previous DMA has drained
+    par_memcpy(c->ring[slot], (const uint8_t*)src + off, len);
+    CK(cudaMemcpyAsync((uint8_t*)dst + off, c->ring[slot], len, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(c->ring_ev[slot], st));
+  }
+  return HTH_OK;
+}
+
 // seed words [0, total) of `fold` in c.seeds, expanded on st unless already there
 int host_seeds(HostCtx* c, u64 fold, u64 total, cudaStream_t st) {
   if (c->seeds_valid >= total && c->seeds_fold == fold) return HTH_OK;
@@ -1123,7 +1170,8 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
     cudaStream_t st = c->st[b];
     const u64 s0 = ch * per, ns = std::min(per, n_strings - s0);
     const uint8_t* src = (const uint8_t*)h_data + s0 * stride_bytes;
-    if (n_bytes) CK(cudaMemcpyAsync(c->buf[b], src, (ns - 1) * stride_bytes + n_bytes, cudaMemcpyHostToDevice, st));
+    if (n_bytes)
+      if (int rc = h2d(c, c->buf[b], src, (ns - 1) * stride_bytes + n_bytes, st)) return rc;
     if (int rc = hth_hash_fixed(output_bytes, c->buf[b], ns, dstride, n_bytes, fold_of(master), c->seeds, lay.total,
                                 c->out + s0 * v.k, c->ws[b], c->ws_bytes, st))
       return rc;
