@@ -542,6 +542,33 @@ def test_host_api_strides_and_capacity(hh):
         hh.hash_fixed_host(host, B, n, bytes(range(32)), p, stride=stride, seed_capacity=5)
 
 
+def test_host_paths_pageable_staging_and_small_calls(hh):
+    # the three host-copy routes of hth_hash_fixed_host: <= 256 KiB calls via
+    # pinned staging on one stream, pageable inputs >= 8 MiB via the parallel
+    # memcpy into pinned slots (several slots, a partial last one), pinned
+    # sources straight to the DMA engine -- all equal to the oracle
+    import torch
+
+    master = bytes(range(32))
+    for w, n in ((24, 100), (40, 200_000), (16, (40 << 20) + 13), (40, (33 << 20) + 5)):
+        p = hh.variant(w)
+        data = o.fill_bytes(n, 11)
+        S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(w), n))
+        want = coracle.hash_one(w, np.frombuffer(data, dtype=np.uint8), S)
+        got = hh.hash_bytes(data, hh.seed_for_input(master, p, n), p)
+        assert tuple(int(x) for x in want) == got.words, (w, n)
+    # a pageable batch whose chunk copies take the staging path, and the same
+    # bytes from pinned memory
+    p = hh.variant(32)
+    n, B = 1 << 20, 24
+    host = np.frombuffer(o.fill_bytes(B * n, 12), dtype=np.uint8).copy()
+    S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(32), n))
+    want = coracle.hash_fixed(32, host, B, n, n, S)
+    assert np.array_equal(hh.hash_fixed_host(host, B, n, master, p), want)
+    pinned = torch.from_numpy(host).pin_memory()
+    assert np.array_equal(hh.hash_fixed_host(pinned, B, n, master, p), want)
+
+
 # ------------------------------------------------------------------ streaming
 @pytest.mark.parametrize("w", (16, 40))
 def test_stream_hasher_matches_one_shot(hh, w):
