@@ -394,17 +394,26 @@ int launch_tail(const TailParams& P, cudaStream_t st) {
   return launch_tail_g<OUT, CPT, MASKED, 1>(P, st);
 }
 
+// chunks per lane of the instantiation that serves nch 16-byte chunks
+inline int tail_cpt(u64 nch) {
+  const u64 cpt = ceil_div(nch, 16);
+  return cpt <= 1 ? 1 : (cpt <= 2 ? 2 : (cpt <= 4 ? 4 : 6));
+}
 template <int OUT, bool MASKED>
 int dispatch_tail_m(const TailParams& P, u64 nch, cudaStream_t st) {
-  const u64 cpt = ceil_div(nch, 16);
-  if (cpt <= 1) return launch_tail<OUT, 1, MASKED>(P, st);
-  if (cpt <= 2) return launch_tail<OUT, 2, MASKED>(P, st);
-  if (cpt <= 4) return launch_tail<OUT, 4, MASKED>(P, st);
+  switch (tail_cpt(nch)) {
+    case 1: return launch_tail<OUT, 1, MASKED>(P, st);
+    case 2: return launch_tail<OUT, 2, MASKED>(P, st);
+    case 4: return launch_tail<OUT, 4, MASKED>(P, st);
+  }
   return launch_tail<OUT, 6, MASKED>(P, st);
 }
 template <int OUT>
 int dispatch_tail(const TailParams& P, u64 nch, cudaStream_t st) {
-  const bool masked = (P.n_bytes % 16) != 0 || (nch % 16) != 0;
+  // the unmasked body processes exactly 16 * CPT whole chunks per string:
+  // anything else (a partial last chunk, or fewer chunks than the
+  // instantiation covers, e.g. 80 chunks on the CPT = 6 body) is masked
+  const bool masked = (P.n_bytes % 16) != 0 || nch != 16ull * tail_cpt(nch);
   return masked ? dispatch_tail_m<OUT, true>(P, nch, st) : dispatch_tail_m<OUT, false>(P, nch, st);
 }
 

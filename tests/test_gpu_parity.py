@@ -109,6 +109,24 @@ def test_tail_only_kernel(hh, w):
 
 
 @pytest.mark.parametrize("w", VARIANTS)
+def test_every_tail_only_length(hh, w):
+    # every length below one instance (0 .. 8m-1 bytes): the tail-only batch
+    # kernel's chunk-count instantiations (1/2/4/6 chunks per lane, masked or
+    # not) must all match the oracle -- e.g. 768 and 1280 B, whose chunk counts
+    # (48, 80) fall short of a whole instantiation
+    iw = o.variant(w).m * 8
+    master = bytes(range(32))
+    p = hh.variant(w)
+    B = 3
+    for n in range(0, iw):
+        host = np.frombuffer(o.fill_bytes(B * max(n, 1), 20 + n), dtype=np.uint8).copy()
+        S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(w), n))
+        want = coracle.hash_fixed(w, host, B, max(n, 1), n, S)
+        got = hh.hash_fixed_host(host, B, n, master, p, stride=max(n, 1))
+        assert np.array_equal(got, want), (w, n)
+
+
+@pytest.mark.parametrize("w", VARIANTS)
 def test_small_string_kernel(hh, w):
     # 1..7 instances with 8-byte-aligned strides take the packed small-string
     # kernel (G = 4/2/1 strings per stage by stride); partial final words in
