@@ -127,6 +127,24 @@ def test_every_tail_only_length(hh, w):
 
 
 @pytest.mark.parametrize("w", VARIANTS)
+def test_every_length_up_to_ten_instances(hh, w):
+    # every length from one instance to ten (the packed small-string kernel
+    # for 1-7 instances with 8-byte-aligned strides, the unaligned job kernel
+    # otherwise, then a partial or complete level-1 group), two strings per
+    # batch: each must match the oracle
+    iw = o.variant(w).m * 8
+    master = bytes(range(32))
+    p = hh.variant(w)
+    for n in range(iw, 10 * iw):
+        S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(w), n))
+        for stride in ((n + 7) // 8 * 8, n + 3):
+            host = np.frombuffer(o.fill_bytes(2 * stride, n), dtype=np.uint8).copy()
+            want = coracle.hash_fixed(w, host, 2, stride, n, S)
+            got = hh.hash_fixed_host(host, 2, n, master, p, stride=stride)
+            assert np.array_equal(got, want), (w, n, stride)
+
+
+@pytest.mark.parametrize("w", VARIANTS)
 def test_small_string_kernel(hh, w):
     # 1..7 instances with 8-byte-aligned strides take the packed small-string
     # kernel (G = 4/2/1 strings per stage by stride); partial final words in
@@ -187,6 +205,27 @@ def test_varlen_packed(hh, w):
     want = coracle.hash_varlen(w, host, off, S)
     bad = np.nonzero(~np.all(got == want, axis=1))[0]
     assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]} offsets {off[bad[:8]] % 16}"
+
+
+@pytest.mark.parametrize("w", VARIANTS)
+def test_varlen_every_length_up_to_ten_instances(hh, w):
+    # one packed batch holding every length 0 .. 10 instances once, shuffled
+    # (unaligned starts): tail-only strings (planning kernel), 1-7 instances
+    # and partial/complete level-1 groups (varlen job kernel)
+    from workloads import offsets_of
+
+    iw = o.variant(w).m * 8
+    lengths = np.random.default_rng(w).permutation(np.arange(10 * iw + 1, dtype=np.int64))
+    off = offsets_of(lengths)
+    total = int(off[-1])
+    buf = hh.fill_bytes(total, 33)
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, int(lengths.max()))
+    got = _u64(hh.hash_varlen(buf, off, seed, p))
+    host = np.frombuffer(o.fill_bytes(total, 33), dtype=np.uint8).copy()
+    want = coracle.hash_varlen(w, host, off, seed.words_np(0, seed.capacity))
+    bad = np.nonzero(~np.all(got == want, axis=1))[0]
+    assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]}"
 
 
 @pytest.mark.parametrize("n_strings", (16384, 16385, 70001))
