@@ -420,6 +420,24 @@ def test_many_seeds_vs_oracle(hh, w):
             assert np.array_equal(got2[b], coracle.hash_one(w, host[s0:s0 + n], S)), (w, n, b, "strided")
 
 
+@pytest.mark.parametrize("w", VARIANTS)
+def test_many_seeds_every_length_up_to_three_instances(hh, w):
+    # the per-seed job kernel (every length goes through hash_kernel with
+    # seeds recomputed from each row's fold), lengths 0 .. 3 instances
+    import torch
+
+    v = o.variant(w)
+    folds = np.array([7, 0xFFFFFFFFFFFFFFFF], dtype=np.uint64)
+    data = np.frombuffer(o.fill_bytes(3 * v.m * 8, 23), dtype=np.uint8).copy()
+    t = torch.from_numpy(data).cuda()
+    p = hh.variant(w)
+    for n in range(0, 3 * v.m * 8):
+        got = _u64(hh.hash_fixed_folds(t, n, folds, p, stride=0))
+        for b in range(2):
+            S = o.splitmix_words(int(folds[b]), 0, o.seed_words_needed(v, n))
+            assert np.array_equal(got[b], coracle.hash_one(w, data[:n], S)), (w, n, b)
+
+
 def test_many_seeds_collision_smoke(hh):
     # GPU-scale version of the reference's seam test (tests/test_hasher.py:263-281):
     # two 2 KB inputs one byte apart under 10^6 seeds -> no colliding digest
