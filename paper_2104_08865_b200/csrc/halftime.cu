@@ -588,6 +588,24 @@ thread_local HostCtx g_host;
 
 int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_bytes, HostCtx** out) {
   HostCtx& c = g_host;
+  if (c.dev >= 0 && c.dev != device) {
+    // this thread moved to another device: release the old device's buffers
+    cudaSetDevice(c.dev);
+    for (int i = 0; i < 3; i++) {
+      if (c.st[i]) cudaStreamDestroy(c.st[i]);
+      if (c.buf[i]) cudaFree(c.buf[i]);
+      if (c.ws[i]) cudaFree(c.ws[i]);
+    }
+    for (int i = 0; i < 2; i++) {
+      if (c.ring[i]) cudaFreeHost(c.ring[i]);
+      if (c.ring_ev[i]) cudaEventDestroy(c.ring_ev[i]);
+    }
+    if (c.seeds) cudaFree(c.seeds);
+    if (c.out) cudaFree(c.out);
+    if (c.hin) cudaFreeHost(c.hin);
+    if (c.hout) cudaFreeHost(c.hout);
+    c = HostCtx();
+  }
   CK(cudaSetDevice(device));
   if (c.dev != device) {
     c = HostCtx();
@@ -1006,13 +1024,17 @@ int hth_ipc_get_handle(const void* d_ptr, uint8_t handle_out[64], uint64_t* offs
   // the handle names the whole allocation (e.g. a caching-allocator segment):
   // report where d_ptr sits inside it
   typedef int (*AddrRange)(unsigned long long*, size_t*, unsigned long long);
+  static std::mutex mu;
   static AddrRange range = nullptr;
-  if (!range) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
-    if (q != cudaDriverEntryPointSuccess || !fn) return fail(HTH_ECUDA, "cuMemGetAddressRange unavailable");
-    range = (AddrRange)fn;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!range) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !fn) return fail(HTH_ECUDA, "cuMemGetAddressRange unavailable");
+      range = (AddrRange)fn;
+    }
   }
   unsigned long long base = 0;
   size_t size = 0;
