@@ -4,6 +4,8 @@ public Python API and the C-ABI underneath) must equal the C oracle's, which
 is pinned to the reference's golden vectors (tests/test_oracle_golden.py).
 Integer work: bit-exact, no tolerance."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -17,7 +19,9 @@ from hypothesis import strategies as stg  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 VARIANTS = (16, 24, 32, 40)
-SETTINGS = dict(max_examples=150, deadline=None, derandomize=True,
+# HTH_HYPOTHESIS_EXAMPLES=N: a longer, non-derandomised exploration run
+_N = int(os.environ.get("HTH_HYPOTHESIS_EXAMPLES", "0"))
+SETTINGS = dict(max_examples=_N or 150, deadline=None, derandomize=not _N,
                 suppress_health_check=[HealthCheck.function_scoped_fixture, HealthCheck.too_slow])
 
 
