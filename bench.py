@@ -630,8 +630,14 @@ def arm_ours(args, rank, world, local_rank):
         runs = [cb.rate() for _ in range(8)]
         cb.close()
         r = statistics.median(x[0] for x in runs)
+        # the same algorithm in one process (single process and all cores)
+        c1 = CpuBaseline(workload, CPU_PER_CORE.get(workload, 4), 1)
+        c1.rate()
+        r1 = statistics.median(c1.rate()[0] for _ in range(3))
+        c1.close()
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": cb.sample() + f"; median of 8 passes, {sum(x[2] for x in runs):.2f} s"}
+               "sample": cb.sample() + f"; median of 8 passes, {sum(x[2] for x in runs):.2f} s",
+               "single_core_value": r1}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
