@@ -604,7 +604,19 @@ def arm_ours(args, rank, world, local_rank):
     e2e = None
     if args.e2e_steps > 0:
         try:
-            e2e, _ = e2e_fixed(hh, torch, workload, args.e2e_steps, args.e2e_strings, rank, world, local_rank, dist)
+            e2e, e2e_out = e2e_fixed(hh, torch, workload, args.e2e_steps, args.e2e_strings, rank, world, local_rank,
+                                     dist)
+            if rank == 0 and not args.no_check:  # the host-path digests of 4 strings against the oracle
+                from oracle import c as coracle
+
+                cfg = wl.CONFIGS[workload]
+                n_ = cfg["n_bytes"]
+                # rank 0's strings: global i (capped batch) or i * world (round-robin shard)
+                gidx = [i if args.e2e_strings else i * world for i in range(4)]
+                host = np.frombuffer(b"".join(wl.host_bytes(g * n_, n_) for g in gidx), np.uint8).copy()
+                seed_ = hh.seed_for_input(wl.MASTER, hh.variant(cfg["variant"]), n_)
+                want = coracle.hash_fixed(cfg["variant"], host, 4, n_, n_, seed_.words_np(0, seed_.capacity))
+                e2e["oracle_check"] = bool(np.array_equal(np.asarray(e2e_out)[:4].view(np.uint64), want))
         except Exception as ex:  # pragma: no cover - report, do not hide
             e2e = {"value": None, "unit": UNIT, "error": repr(ex), "h2d_bytes_per_step": None,
                    "d2h_bytes_per_step": None}

@@ -644,6 +644,29 @@ def test_host_paths_pageable_staging_and_small_calls(hh):
     assert np.array_equal(hh.hash_fixed_host(pinned, B, n, master, p), want)
 
 
+def test_host_batch_many_chunks(hh):
+    # hth_hash_fixed_host cuts a large batch into ~64 MiB chunks over three
+    # streams and three device buffers (reused from the fourth chunk on), and
+    # copies the digests back once: 260 x 1 MiB (5 chunks, a short last one)
+    # from pageable and from pinned memory, against the oracle
+    import torch
+
+    master = bytes(range(32))
+    p = hh.variant(40)
+    n, B = (1 << 20) + 40, 260
+    stride = n + 24
+    host = np.frombuffer(o.fill_bytes(B * stride, 31), dtype=np.uint8).copy()
+    S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(40), n))
+    want = coracle.hash_fixed(40, host, B, stride, n, S)
+    got = hh.hash_fixed_host(host, B, n, master, p, stride=stride)
+    bad = np.nonzero(~np.all(got == want, axis=1))[0]
+    assert bad.size == 0, f"pageable: {bad.size} mismatches, first {bad[:8]}"
+    pinned = torch.from_numpy(host).pin_memory()
+    got = hh.hash_fixed_host(pinned, B, n, master, p, stride=stride)
+    bad = np.nonzero(~np.all(got == want, axis=1))[0]
+    assert bad.size == 0, f"pinned: {bad.size} mismatches, first {bad[:8]}"
+
+
 # ------------------------------------------------------------------ streaming
 @pytest.mark.parametrize("w", (16, 40))
 def test_stream_hasher_matches_one_shot(hh, w):
