@@ -57,3 +57,61 @@ def test_c_program_against_the_shared_library(tmp_path):
         assert words == o.seed_words_needed(o.variant(w), n), line
     assert lines[28] == f"fold {o.master_fold(bytes(range(32)))}"
     assert lines[29].startswith("err ") and len(lines[29]) > 4
+
+
+GPU_PROGRAM = r"""
+#include <stdio.h>
+#include <stdlib.h>
+#include <cuda_runtime.h>
+#include "halftime_b200.h"
+/* config 1's shape: 1024 strings x 4096 B, 24-byte digests, through the C-ABI
+ * only (device buffers, one stream), data read from stdin */
+int main(void) {
+  const uint64_t B = 1024, n = 4096, k = 3;
+  uint8_t* h = (uint8_t*)malloc(B * n);
+  if (fread(h, 1, B * n, stdin) != B * n) return 2;
+  uint8_t master[32];
+  for (int i = 0; i < 32; i++) master[i] = (uint8_t)(7 * i + 1);
+  uint64_t fold, cap, ws_bytes;
+  if (hth_master_fold(master, &fold) || hth_seed_words_needed(24, n, &cap) ||
+      hth_workspace_size_fixed(24, B, n, &ws_bytes)) return 3;
+  void *d_data, *ws; uint64_t *d_seed, *d_out;
+  cudaMalloc(&d_data, B * n); cudaMalloc(&ws, ws_bytes); cudaMemset(ws, 0, ws_bytes);
+  cudaMalloc((void**)&d_seed, cap * 8); cudaMalloc((void**)&d_out, B * k * 8);
+  cudaMemcpy(d_data, h, B * n, cudaMemcpyHostToDevice);
+  cudaStream_t st; cudaStreamCreate(&st);
+  if (hth_expand_seed(fold, 0, cap, d_seed, st)) return 4;
+  int rc = hth_hash_fixed(24, d_data, B, n, n, fold, d_seed, cap, d_out, ws, ws_bytes, st);
+  if (rc) { fprintf(stderr, "%s\n", hth_last_error()); return 5; }
+  uint64_t* out = (uint64_t*)malloc(B * k * 8);
+  cudaMemcpyAsync(out, d_out, B * k * 8, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  fwrite(out, 8, B * k, stdout);
+  return 0;
+}
+"""
+
+
+@pytest.mark.gpu
+def test_c_program_hashes_on_the_gpu(tmp_path):
+    import numpy as np
+
+    from oracle import c as coracle
+
+    cuda = "/usr/local/cuda"
+    src = tmp_path / "abi_gpu.c"
+    src.write_text(GPU_PROGRAM)
+    exe = tmp_path / "abi_gpu"
+    libdir = os.path.dirname(LIB)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", f"{cuda}/include",
+                    str(src), "-L", libdir, "-l:libhalftime_b200.so", f"-Wl,-rpath,{libdir}",
+                    "-L", f"{cuda}/lib64", "-lcudart", f"-Wl,-rpath,{cuda}/lib64", "-o", str(exe)], check=True)
+    rng = np.random.default_rng(17)
+    data = rng.integers(0, 256, 1024 * 4096, dtype=np.uint8)
+    r = subprocess.run([str(exe)], input=data.tobytes(), capture_output=True)
+    assert r.returncode == 0, r.stderr
+    got = np.frombuffer(r.stdout, dtype=np.uint64).reshape(1024, 3)
+    master = bytes((7 * i + 1) & 0xFF for i in range(32))
+    S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(24), 4096))
+    want = coracle.hash_fixed(24, data, 1024, 4096, 4096, S)
+    assert np.array_equal(got, want)
