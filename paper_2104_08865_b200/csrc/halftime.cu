@@ -184,6 +184,11 @@ __global__ void __launch_bounds__(256) plan_tail_kernel(const __grid_constant__ 
   constexpr int NKEY = M + K;  // Toeplitz keys R .. R + m + k - 2, plus slack
   __shared__ u64 key[NKEY];
   __shared__ u64 tagseed[K];
+  // this half-warp's first string bounds, loaded before the key staging so
+  // the two latencies overlap
+  const u64 s_first = (u64)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4);
+  const u64 f_o0 = s_first < P.n ? P.off[s_first] : 0;
+  const u64 f_o1 = s_first < P.n ? P.off[s_first + 1] : 0;
   for (int i = threadIdx.x; i < NKEY; i += blockDim.x) key[i] = __ldg(P.S + P.R + i);
   if (threadIdx.x < K) tagseed[threadIdx.x] = __ldg(P.S + P.F0 + 64ull * threadIdx.x);
   // zero-slot table: one thread per (L, l, r) sums its 7 slots and writes the
@@ -220,8 +225,9 @@ __global__ void __launch_bounds__(256) plan_tail_kernel(const __grid_constant__ 
   // both halves of a warp iterate together (the reduction shuffles are warp-wide)
   for (u64 s = (u64)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); s < ((P.n + 1) & ~1ull); s += halves) {
     const bool live = s < P.n;
-    const u64 o0 = live ? P.off[s] : 0;
-    u64 n = live ? P.off[s + 1] - o0 : 0;
+    const bool first = s == s_first;
+    const u64 o0 = live ? (first ? f_o0 : P.off[s]) : 0;
+    u64 n = live ? (first ? f_o1 : P.off[s + 1]) - o0 : 0;
     if (n > P.max_n) {
       if (g == 0) atomicOr(P.err, 1);
       n = P.max_n;

@@ -286,16 +286,22 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
                                         (PS ? W * 2 * MAX_EW * 4 : 0));
   u64 n_jobs = P.n_jobs;
   if (VARLEN) {
-    for (int c = threadIdx.x; c < NCLS; c += blockDim.x) cls_pre[c] = c ? P.cls_cnt[c] : 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      u32 acc = 0;
-      for (int c = NCLS - 1; c >= 1; c--) {
-        const u32 k = cls_pre[c];
-        cls_pre[c] = acc;
-        acc += k;
+    // cls_pre[c] = jobs in classes > c (c >= 1), cls_pre[0] = all jobs: a
+    // suffix scan of the 64 class counts by warp 0, two classes per lane
+    static_assert(NCLS == 65, "two size classes per lane of one warp");
+    if (warp == 0) {
+      const int c1 = 2 * lane + 1, c2 = c1 + 1;
+      const u32 a = P.cls_cnt[c1], b = P.cls_cnt[c2];
+      u32 x = a + b;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 t = __shfl_down_sync(0xffffffffu, x, d);
+        if (lane + d < 32) x += t;
       }
-      cls_pre[0] = acc;
+      const u32 above = x - (a + b);  // classes > c2
+      cls_pre[c2] = above;
+      cls_pre[c1] = above + b;
+      if (lane == 0) cls_pre[0] = x;
     }
     __syncthreads();
     n_jobs = cls_pre[0];
