@@ -129,3 +129,79 @@ def test_hash_varlen_random(hh, case):
     want = coracle.hash_varlen(w, host, off, _seeds(master, w, mx))
     bad = np.nonzero(~np.all(got == want, axis=1))[0]
     assert bad.size == 0, (w, [lengths[i] for i in bad[:5]])
+
+
+@stg.composite
+def folds_batch(draw):
+    w = draw(stg.sampled_from(VARIANTS))
+    n = _length(draw, w) % 30000
+    B = draw(stg.integers(1, 40))
+    shared = draw(stg.booleans())  # one input under every fold (stride 0) or distinct inputs
+    return w, n, B, shared, draw(stg.integers(0, 2**31))
+
+
+@settings(**SETTINGS)
+@given(folds_batch())
+def test_many_seeds_random(hh, case):
+    # hth_hash_fixed_folds: row s hashed under the seed stream of folds[s]
+    # (the reference seam with a (B, 1) fold region, tests/test_hasher.py:254-310)
+    w, n, B, shared, ms = case
+    rng = np.random.default_rng(ms)
+    folds = rng.integers(0, 1 << 64, size=B, dtype=np.uint64)
+    stride = 0 if shared else (n + 15) // 16 * 16
+    total = max(n if shared else B * stride, 16)
+    p = hh.variant(w)
+    buf = hh.fill_bytes(total, ms & 0xFFFF)
+    got = hh.hash_fixed_folds(buf, n, folds, p, stride=max(stride, 0)).cpu().numpy().view(np.uint64)
+    host = np.frombuffer(o.fill_bytes(total, ms & 0xFFFF), dtype=np.uint8).copy()
+    v = o.variant(w)
+    for b in range(B):
+        s0 = 0 if shared else b * stride
+        S = o.splitmix_words(int(folds[b]), 0, o.seed_words_needed(v, n))
+        assert np.array_equal(got[b], coracle.hash_one(w, host[s0:s0 + n], S)), (w, n, b)
+
+
+@stg.composite
+def split_string(draw):
+    w = draw(stg.sampled_from(VARIANTS))
+    iw = o.variant(w).m * 8
+    inst = draw(stg.sampled_from([0, 1, 63, 64, 65, 511, 512, 513, 600, 4096, 4097, 5000, 33000]))
+    n = inst * iw + draw(stg.integers(0, iw - 1))
+    return w, n, draw(stg.integers(1, 9)), draw(stg.integers(0, 2**31))
+
+
+@settings(**dict(SETTINGS, max_examples=min(SETTINGS["max_examples"], 400)))
+@given(split_string())
+def test_split_string_and_stream_random(hh, case):
+    # one string cut into ns slices (emulated ranks, one after another) and
+    # merged, and the same bytes fed to StreamHasher in random pieces: both
+    # equal the oracle's one-shot digest
+    import torch
+
+    from paper_2104_08865_b200 import multi_gpu
+
+    w, n, ns, ms = case
+    p = hh.variant(w)
+    master = _master(ms)
+    seed = hh.seed_for_input(master, p, n)
+    buf = hh.fill_bytes(max(n, 16), ms & 0xFFFF)
+    host = np.frombuffer(o.fill_bytes(max(n, 16), ms & 0xFFFF), dtype=np.uint8)[:n].copy()
+    want = coracle.hash_one(w, host, _seeds(master, w, n))
+    if n >= 512 * o.variant(w).m * 8:  # the split needs whole level-c subtrees (c >= the job level)
+        plan = multi_gpu.slice_plan(p, n, ns)
+        frs, parts = [], []
+        for i in range(ns):
+            b0, _ = plan.byte_range(i)
+            fr, part = multi_gpu.hash_slice(buf[b0:], plan, i, seed)
+            frs.append(fr.clone())
+            parts.append(part.clone())
+        got = multi_gpu.hash_merge(torch.cat(frs), torch.stack(parts), plan, seed)
+        assert np.array_equal(got.cpu().numpy().view(np.uint64), want), (w, n, ns)
+    h = hh.StreamHasher(p, seed, n, slice_bytes=1 << 20)
+    rng = np.random.default_rng(ms)
+    pos = 0
+    while pos < n:
+        step = int(rng.integers(1, max(2, n // 3 + 2)))
+        h.update(host[pos:pos + step].tobytes())
+        pos += step
+    assert tuple(int(x) for x in want) == tuple(h.digest().words), (w, n, "stream")
