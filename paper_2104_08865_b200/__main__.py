@@ -1,17 +1,21 @@
-"""Command line served by the CUDA engine: ``hash`` and ``vectors``.
+"""Command line served by the CUDA engine: ``hash``, ``bench`` and ``vectors``.
 
-Mirrors the reference's front end (halftimehash/cli.py:78-84 ``hash``,
-189-222 ``vectors``) for the hash path only; analysis/verify/bench are out of
-scope.  Exit codes follow cli.py:263-273: 0 ok, 1 check failure, 2 usage/IO.
+Mirrors the reference's front end for its hash-path commands
+(halftimehash/cli.py:78-84 ``hash``, 169-186 ``bench``, 189-222 ``vectors``);
+analyze/verify are out of scope.  Exit codes follow cli.py:263-273: 0 ok,
+1 check failure, 2 usage/IO.
 
   python -m paper_2104_08865_b200 hash [--variant 24] [--seed-hex HEX | --seed-file F] [FILE|-]
+  python -m paper_2104_08865_b200 bench [--sizes 1K,256K,1M] [--reps 5]
   python -m paper_2104_08865_b200 vectors (--emit PATH | --check PATH)
 """
 
 from __future__ import annotations
 
 import argparse
+import statistics
 import sys
+import time
 
 import numpy as np
 
@@ -65,6 +69,48 @@ def _fill(n: int) -> bytes:
     return fill_bytes(n, FILL_SEED).cpu().numpy()[:n].tobytes()
 
 
+_SIZE_SUFFIXES = {"K": 1, "M": 2, "G": 3, "T": 4, "P": 5, "E": 6}  # cli.py:20
+
+
+def parse_size(text: str) -> int:
+    """'1K' -> 1024 (cli.py:33-45)."""
+    text = text.strip()
+    if not text:
+        raise argparse.ArgumentTypeError("empty size")
+    mult = 1
+    if text[-1].upper() in _SIZE_SUFFIXES:
+        mult = 1024 ** _SIZE_SUFFIXES[text[-1].upper()]
+        text = text[:-1]
+    try:
+        value = int(text)
+    except ValueError:
+        raise argparse.ArgumentTypeError(f"bad size {text!r}") from None
+    return value * mult
+
+
+def cmd_bench(args) -> int:
+    """Report-only throughput of ``hash_bytes`` per size and variant, in the
+    reference's CSV (cli.py:169-186): median of ``reps`` timed calls after one
+    warm-up call, wall clock around the public one-shot API (host bytes in,
+    Digest out).  The cycle column stays empty, as in the reference."""
+    sizes = [parse_size(s) for s in args.sizes.split(",")]
+    print("size_bytes,variant,bytes_per_second,bytes_per_cycle")
+    for size in sizes:
+        data = _fill(size)
+        for width in sorted(VARIANTS):
+            params = variant(width)
+            seed = hasher.seed_for_input(b"\x00" * 32, params, size)
+            hasher.hash_bytes(data, seed, params)  # warm-up
+            rates = []
+            for _ in range(args.reps):
+                t0 = time.perf_counter()
+                hasher.hash_bytes(data, seed, params)
+                dt = time.perf_counter() - t0
+                rates.append(size / dt if dt > 0 else float("inf"))
+            print(f"{size},{width},{statistics.median(rates):.0f},")
+    return 0
+
+
 def vector_records():
     datas = {n: _fill(n) for n in VECTOR_LENGTHS}
     for width in sorted(VARIANTS):
@@ -106,6 +152,10 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--seed-file")
     p.add_argument("input", nargs="?")
     p.set_defaults(func=cmd_hash)
+    p = sub.add_parser("bench", help="report-only throughput benchmark")
+    p.add_argument("--sizes", default="1K,256K,1M")
+    p.add_argument("--reps", type=int, default=5)
+    p.set_defaults(func=cmd_bench)
     p = sub.add_parser("vectors", help="emit or check the golden vector file")
     g = p.add_mutually_exclusive_group(required=True)
     g.add_argument("--emit", metavar="PATH")

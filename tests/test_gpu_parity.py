@@ -481,6 +481,22 @@ def test_cli_hash_empty_stdin(hh, monkeypatch, capsys):
     assert main(["hash", "--seed-hex", "00"]) == 2
 
 
+def test_cli_bench_csv_contract(hh, capsys):
+    # the reference's bench CSV contract (pkg/tests/test_cli.py:117-129)
+    from paper_2104_08865_b200.__main__ import main
+
+    assert main(["bench", "--sizes", "1K,4K", "--reps", "2"]) == 0
+    lines = capsys.readouterr().out.strip().splitlines()
+    assert lines[0] == "size_bytes,variant,bytes_per_second,bytes_per_cycle"
+    rows = [line.split(",") for line in lines[1:]]
+    assert len(rows) == 2 * 4
+    for size, width, bps, bpc in rows:
+        assert int(size) in (1024, 4096)
+        assert int(width) in (16, 24, 32, 40)
+        assert float(bps) > 0
+        assert bpc == ""
+
+
 # ------------------------------------------------------------------ edge cases
 def test_empty_batches_and_zero_length(hh):
     import torch
