@@ -4,8 +4,9 @@
 * criterion 7 (:168-186): no digest collisions over 10^5 random 2 KB inputs
   per variant -- here all 10^5 inputs of a variant are one batch through the
   CUDA engine, and a sample is also checked against the C oracle;
-* the engine-agreement sweep (:189-220): 2,500 random (length, master) pairs
-  per variant through the public ``hash_bytes`` against the C oracle (the
+* the engine-agreement sweep (criterion 8, :189-220): 2,500 (length, master)
+  pairs per variant with its boundary-heavy length mix (+250 longer strings)
+  through the public ``hash_bytes`` against the C oracle (the
   reference compares its scalar and lanes engines; the oracle is pinned to
   both through the golden digests, tests/test_oracle_golden.py).
 Integer work: bit-exact, no tolerance.
@@ -52,9 +53,15 @@ def test_criterion7_no_collisions_1e5_random_2kb(hh, w):
 
 @pytest.mark.parametrize("w", VARIANTS)
 def test_random_length_master_pairs_2500(hh, w):
+    # criterion 8's mix (test_acceptance.py:189-200): the instance/block
+    # boundary lengths 40 times each, the rest uniform in [0, 2 instances),
+    # plus 250 longer strings (multi-round and multi-job paths)
     rng = np.random.default_rng(2500 + w)
     p = hh.variant(w)
-    lengths = np.concatenate([rng.integers(0, 4096, 2000), rng.integers(4096, 200_000, 500)])
+    iw = o.variant(w).m * 8
+    boundary = [0, 1, 63, 64, 65, iw - 8, iw - 1, iw, iw + 1, iw + 8, 2 * iw - 1, 2 * iw, 2 * iw + 1]
+    lengths = np.concatenate([np.array(boundary * 40), rng.integers(0, 2 * iw, 2500 - 40 * len(boundary)),
+                              rng.integers(2 * iw, 200_000, 250)])
     for i, n in enumerate(lengths.tolist()):
         master = rng.integers(0, 256, 32, dtype=np.uint8).tobytes()
         data = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
