@@ -161,10 +161,14 @@ int hth_ipc_open_handle(const uint8_t handle[64], void** d_ptr_out);
 int hth_ipc_close_handle(void* d_ptr);
 
 /* ---- host-buffer entry points (end-to-end; synchronous).  These are what
- * hash_bytes(..., engine="cuda") binds: host bytes in, host digest words
- * out, seeds expanded on the device from the 32-byte master.  The batch
- * form pipelines host->device copies against hashing in chunks on two
- * streams; pinned (page-locked) h_data gives full PCIe/NVLink-C2C rate.
+ * hash_bytes(..., engine="cuda") binds (hasher.py:434-453): host bytes in,
+ * host digest words out, seeds expanded on the device from the 32-byte
+ * master (cached per calling thread while the master stays the same).
+ * Calls up to 256 KiB run on one stream through pinned staging; larger ones
+ * pipeline ~64 MiB chunks of whole strings over three streams (copy of chunk
+ * i+1 against the hash of chunk i).  Pinned (page-locked) h_data goes
+ * straight to the copy engine at the full PCIe rate; pageable h_data >= 8 MiB
+ * is staged through pinned slots by a multi-threaded memcpy.
  * seed_capacity emulates SeedBuffer.capacity: HTH_ESEEDSIZE if it is below
  * seed_words_needed (0 = size it exactly, like seed_for_input). */
 int hth_hash_host(int output_bytes, const void* h_data, uint64_t n_bytes, const uint8_t master[32],
