@@ -16,8 +16,10 @@
 // the two instances are packed plane-by-plane into shared 32-bit registers
 // so every XOR of the encode advances 32 GF(16) elements.
 // Level-1 nodes (nh.py:96-121) are reduced over the 4 threads sharing j
-// with two shuffles; levels 2..L accumulate serially in lanes 0-7; levels
-// >= L use a "last arriver" merge through a global scratch area.
+// with two shuffles and parked in shared memory; every 8th round the whole
+// warp forms the level-2 node from the 8 parked blocks the same way; a
+// level-3 node (job_lvl 3) accumulates in shared memory; levels >= job_lvl
+// use a "last arriver" merge through a global scratch area.
 //
 // The reference's finalize (tree.py:103-134) is a plain sum of NH terms
 // over leftover slots, zero slots and the length tag; the tail is a sum of
