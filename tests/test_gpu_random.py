@@ -170,7 +170,7 @@ def split_string(draw):
     return w, n, draw(stg.integers(1, 9)), draw(stg.integers(0, 2**31))
 
 
-@settings(**dict(SETTINGS, max_examples=min(SETTINGS["max_examples"], 400)))
+@settings(**dict(SETTINGS, max_examples=_N // 10 if _N else 150))
 @given(split_string())
 def test_split_string_and_stream_random(hh, case):
     # one string cut into ns slices (emulated ranks, one after another) and
