@@ -382,6 +382,10 @@ def measure_workload(hh, torch, workload, steps, warmup, peak):
     res.update(value=gbs, ms_per_step=ms, bytes_per_step=ctx["B"] * ctx["n"],
                roofline_frac=(algo / (ms / 1e3) / 1e9) / peak,
                l2="flushed before every timed step" if flush else "inputs larger than L2 (126 MB)")
+    if workload == "cfg1":
+        res["bound"] = ("latency: one launch hashes 4 MiB (0.6 us of HBM time); each warp's critical path is "
+                        "one stage's DRAM round trip after the flush + one two-instance leaf + finalize "
+                        "(profiles/README.md)")
     del ctx
     torch.cuda.empty_cache()
     return res
