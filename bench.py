@@ -369,7 +369,10 @@ def measure_workload(hh, torch, workload, steps, warmup, peak):
         res.update(value=4 * total / (ms / 1e3) / 1e9, ms_per_step=ms, bytes_per_step=4 * total,
                    l2="flushed (256 MB write) before every timed step",
                    execution="4 variants on 4 forked streams, captured as one CUDA graph, replayed per step",
-                   graph_matches_serial=same)
+                   graph_matches_serial=same,
+                   bound=("latency: ~10 us fixed per variant call (workspace clear + planning kernel + hash "
+                          "kernel launch) and ~3 us per warp job (claim, decode, finalize) against ~2.5 us "
+                          "rounds; 98 MB per variant is 15 us of HBM time (DESIGN.md section 5)"))
         del buf
         return res
     ctx = setup_fixed(hh, torch, workload)
