@@ -683,6 +683,39 @@ def test_host_batch_many_chunks(hh):
     assert bad.size == 0, f"pinned: {bad.size} mismatches, first {bad[:8]}"
 
 
+def test_host_api_from_many_threads(hh):
+    # hash_bytes / hash_fixed_host from 8 Python threads at once (ctypes drops
+    # the GIL; each thread gets its own host context, streams and staging):
+    # every digest equals the oracle's
+    import threading
+
+    master = bytes(range(32))
+    errors = []
+
+    def worker(t):
+        try:
+            rng = np.random.default_rng(900 + t)
+            for _ in range(40):
+                w = int(rng.choice([16, 24, 32, 40]))
+                n = int(rng.choice([0, 7, 999, 5000, 70_000, 300_000, 9 << 20]))
+                data = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+                p = hh.variant(w)
+                got = hh.hash_bytes(data, hh.seed_for_input(master, p, n), p)
+                S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(w), n))
+                want = coracle.hash_one(w, np.frombuffer(data, dtype=np.uint8), S)
+                if tuple(int(x) for x in want) != got.words:
+                    errors.append((t, w, n))
+        except Exception as ex:  # pragma: no cover - surfaced below
+            errors.append((t, repr(ex)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(8)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[:5]
+
+
 # ------------------------------------------------------------------ streaming
 @pytest.mark.parametrize("w", (16, 40))
 def test_stream_hasher_matches_one_shot(hh, w):
