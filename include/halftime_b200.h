@@ -20,10 +20,11 @@
  *      HTH_ECUDA / HTH_ENOMEM -> RuntimeError / MemoryError
  *  - Device entry points are stream-ordered on `stream` (a cudaStream_t,
  *    NULL = legacy default stream) and asynchronous.
- *  - Device input buffers must be 16-byte aligned at their base and
- *    readable up to the next 16-byte boundary past their last byte (TMA
- *    bulk copies move 16-byte granules).  Any cudaMalloc / torch
- *    allocation satisfies this.
+ *  - Device input buffers may start at any byte address.  The engine reads
+ *    whole 16-byte granules (TMA bulk copies), i.e. from the granule holding
+ *    the first byte to the one holding the last; those never cross a page
+ *    boundary, so any cudaMalloc / torch allocation (or view into one) is
+ *    safe.
  *  - Digests are written as n_strings x k little-endian u64 words,
  *    k = output_bytes / 8 (Digest.words, hasher.py:165-176).
  *  - hth_hash_fixed workspaces must be zero-filled before their first use
@@ -57,6 +58,10 @@ extern "C" {
 #define HTH_ERANGE (-3)
 #define HTH_ECUDA (-4)
 #define HTH_ENOMEM (-5)
+
+/* seed_capacity of the host entry points: size the seed stream exactly
+ * (seed_for_input, hasher.py:160-162) instead of checking a capacity. */
+#define HTH_SEED_AUTO UINT64_MAX
 
 /* Last error message of the calling thread ("" if none). */
 const char* hth_last_error(void);
@@ -119,9 +124,15 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
                     uint64_t seed_capacity, uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes,
                     void* stream);
 /* Synchronizes `stream`; returns HTH_ESEEDSIZE if the last varlen call on this
- * workspace met a string longer than its max_n_bytes, HTH_EINVAL if the
- * strings held more bytes than its total_bytes declared, else HTH_OK. */
+ * workspace met a string longer than its max_n_bytes, HTH_EINVAL if offsets
+ * decreased or ran past total_bytes, else HTH_OK (the reference raises
+ * SeedSizeError / ValueError for these, hasher.py:209-214). */
 int hth_varlen_status(void* d_workspace, void* stream);
+
+/* Re-zero a workspace (stream-ordered).  The device entry points already do
+ * this themselves when a launch fails; callers that abandon a workspace
+ * mid-stream (e.g. after an error of their own) can use it too. */
+int hth_workspace_reset(void* d_workspace, uint64_t workspace_bytes, void* stream);
 
 /* ---- one string split across devices (config 5): the reference's stack
  * construction is front-aligned (tree.py:63-100), so a string cut at
@@ -169,13 +180,20 @@ int hth_ipc_close_handle(void* d_ptr);
  * i+1 against the hash of chunk i).  Pinned (page-locked) h_data goes
  * straight to the copy engine at the full PCIe rate; pageable h_data >= 8 MiB
  * is staged through pinned slots by a multi-threaded memcpy.
+ * Strings longer than 64 MiB are streamed in 64 MiB slices of whole
+ * subtrees (hth_hash_slice + hth_hash_merge), so device memory stays bounded
+ * (about 3 x 64 MiB) whatever the input size.
  * seed_capacity emulates SeedBuffer.capacity: HTH_ESEEDSIZE if it is below
- * seed_words_needed (0 = size it exactly, like seed_for_input). */
+ * seed_words_needed (HTH_SEED_AUTO = size it exactly, like seed_for_input).
+ * Each calling thread keeps its streams and buffers for reuse until it exits
+ * or calls hth_host_release. */
 int hth_hash_host(int output_bytes, const void* h_data, uint64_t n_bytes, const uint8_t master[32],
                   uint64_t seed_capacity, uint64_t* h_out, int device);
 int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings, uint64_t stride_bytes,
                         uint64_t n_bytes, const uint8_t master[32], uint64_t seed_capacity, uint64_t* h_out,
                         int device);
+/* Free the calling thread's host-path streams and buffers (device and pinned). */
+int hth_host_release(void);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,7 @@ fallback.
 
 from ._errors import SeedSizeError
 from .hasher import (
+    ENGINES,
     Digest,
     SeedBuffer,
     SeedLayout,
@@ -22,7 +23,15 @@ from .hasher import (
     seed_layout,
     seed_words_needed,
 )
-from .params import VARIANTS, ErasureCode, HashParams, TransformMatrix, variant
+from .params import (
+    SUPPORTED_COEFFICIENTS,
+    VARIANTS,
+    ErasureCode,
+    HashParams,
+    TransformMatrix,
+    coefficient_multiply,
+    variant,
+)
 
 __version__ = "0.1.0"
 
@@ -30,7 +39,8 @@ __all__ = [
     "Digest", "ErasureCode", "HashParams", "SeedBuffer", "SeedLayout", "SeedSizeError", "TransformMatrix",
     "VARIANTS", "digest", "expand_seed", "hash_bytes", "instance_count", "seed_for_input", "seed_layout",
     "seed_words_needed", "variant", "hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes",
-    "hash_fixed_folds", "hash_words_many_seeds", "StreamHasher",
+    "hash_fixed_folds", "hash_words_many_seeds", "StreamHasher", "varlen_status", "release_host", "ENGINES",
+    "SUPPORTED_COEFFICIENTS", "coefficient_multiply",
     "__version__",
 ]
 
@@ -38,7 +48,7 @@ __all__ = [
 def __getattr__(name):
     # batch entry points import torch lazily so host-only use stays light
     if name in ("hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes", "hash_fixed_folds",
-                "hash_words_many_seeds"):
+                "hash_words_many_seeds", "varlen_status", "release_host"):
         from . import batch
 
         return getattr(batch, name)

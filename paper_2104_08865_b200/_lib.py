@@ -24,8 +24,12 @@ EXPORTS = (
     "hth_workspace_size_fixed", "hth_hash_fixed", "hth_workspace_size_varlen",
     "hth_hash_varlen", "hth_varlen_status", "hth_hash_host", "hth_hash_fixed_host",
     "hth_slice_plan", "hth_workspace_size_slice", "hth_hash_slice", "hth_hash_merge", "hth_hash_fixed_folds",
-    "hth_ipc_get_handle", "hth_ipc_open_handle", "hth_ipc_close_handle",
+    "hth_ipc_get_handle", "hth_ipc_open_handle", "hth_ipc_close_handle", "hth_host_release",
+    "hth_workspace_reset",
 )
+
+#: seed_capacity sentinel of the host entry points (HTH_SEED_AUTO)
+SEED_AUTO = (1 << 64) - 1
 
 _lock = threading.Lock()
 _lib = None
@@ -71,6 +75,8 @@ def lib() -> ctypes.CDLL:
             "hth_ipc_get_handle": [vp, vp, pu64],
             "hth_ipc_open_handle": [vp, ctypes.POINTER(ctypes.c_void_p)],
             "hth_ipc_close_handle": [vp],
+            "hth_host_release": [],
+            "hth_workspace_reset": [vp, u64, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)

@@ -19,8 +19,8 @@ from . import _lib
 from .hasher import SeedBuffer, _check_capacity, _check_params, seed_words_needed
 from .params import HashParams
 
-__all__ = ["hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes", "workspace_fixed",
-           "workspace_varlen", "hash_fixed_folds", "hash_words_many_seeds"]
+__all__ = ["hash_fixed", "hash_varlen", "varlen_status", "hash_words", "hash_fixed_host", "fill_bytes",
+           "workspace_fixed", "workspace_varlen", "hash_fixed_folds", "hash_words_many_seeds", "release_host"]
 
 
 def _stream(dev) -> int:
@@ -69,6 +69,22 @@ class _Workspace:
             self.buf[key] = t
         return t
 
+    def drop(self, dev):
+        """Forget this stream's workspace after a failed call: the next call
+        starts from a fresh zero-filled one (the engine also re-zeroes a
+        workspace whose launch failed)."""
+        self.buf.pop((dev.index, _stream(dev)), None)
+
+
+def _call(cache, dev, rc_fn):
+    """Run one C-ABI call; on any error drop the cached workspace, then raise."""
+    try:
+        _lib.check(rc_fn())
+    except Exception:
+        if cache is not None:
+            cache.drop(dev)
+        raise
+
 
 _WS = _Workspace()       # hash_fixed: zero-filled, kept zero by the engine
 _WS_VAR = _Workspace()   # hash_varlen: plan areas are scratch, cleared per call
@@ -106,7 +122,7 @@ def hash_fixed(data: torch.Tensor, n_bytes: int, seed, params: HashParams, n_str
     wsz = workspace_fixed(params, n_strings, n_bytes)
     ws = workspace if workspace is not None else (_WS.get(dev, wsz) if wsz else None)
     with torch.cuda.device(dev):
-        _lib.check(_lib.lib().hth_hash_fixed(
+        _call(_WS if workspace is None else None, dev, lambda: _lib.lib().hth_hash_fixed(
             params.output_bytes, data.data_ptr(), n_strings, stride, n_bytes, fold, seed_t.data_ptr(), cap,
             out.data_ptr(), ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
             _stream(dev)))
@@ -114,17 +130,32 @@ def hash_fixed(data: torch.Tensor, n_bytes: int, seed, params: HashParams, n_str
 
 
 def hash_varlen(data: torch.Tensor, offsets, seed, params: HashParams, max_n_bytes: int = None,
-                out: torch.Tensor = None, workspace: torch.Tensor = None) -> torch.Tensor:
+                out: torch.Tensor = None, workspace: torch.Tensor = None, check: bool = None) -> torch.Tensor:
     """Hash strings ``data[offsets[s]:offsets[s+1]]`` (packed, any alignment).
 
     ``offsets``: n+1 byte offsets, numpy array or CUDA int64 tensor.  With
-    a numpy array the exact longest length is used for the seed check;
-    with a device tensor pass ``max_n_bytes`` (default: the buffer size).
+    a numpy array the offsets are validated and the exact longest length is
+    used for the seed check on the host; with a device tensor pass
+    ``max_n_bytes`` (default: the buffer size) and the device validates them.
+
+    ``check``: read the device's verdict after the call (one stream
+    synchronize) and raise like the reference -- ``SeedSizeError`` if a
+    string is longer than ``max_n_bytes`` (hasher.py:209-214), ``ValueError``
+    for decreasing offsets or offsets past the buffer.  Default: on whenever
+    the host could not validate (device offsets or a caller-supplied
+    ``max_n_bytes``).  Pass ``False`` inside CUDA-graph capture and call
+    ``varlen_status(workspace)`` afterwards.
     """
     params = _check_params(params)
     if not isinstance(data, torch.Tensor) or not data.is_cuda:
         raise ValueError("data must be a CUDA tensor")
+    if data.dtype != torch.uint8:
+        data = data.view(torch.uint8) if data.is_contiguous() else data.contiguous().view(torch.uint8)
+    if data.dim() != 1:
+        data = data.reshape(-1)
     dev = data.device
+    if check is None:
+        check = isinstance(offsets, torch.Tensor) or max_n_bytes is not None
     if isinstance(offsets, torch.Tensor):
         d_off = offsets.to(device=dev, dtype=torch.int64)
         if max_n_bytes is None:
@@ -147,11 +178,23 @@ def hash_varlen(data: torch.Tensor, offsets, seed, params: HashParams, max_n_byt
     total = data.numel()
     wsz = workspace_varlen(params, max(n, 0), total)
     ws = workspace if workspace is not None else _WS_VAR.get(dev, wsz)
+    if workspace is not None and workspace.numel() < wsz:
+        raise ValueError(f"workspace too small: {workspace.numel()} < {wsz} bytes")
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().hth_hash_varlen(
             params.output_bytes, data.data_ptr(), d_off.data_ptr(), n, max_n_bytes, total, fold, seed_t.data_ptr(),
             cap, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(dev)))
+        if check and n > 0:
+            _lib.check(_lib.lib().hth_varlen_status(ws.data_ptr(), _stream(dev)))
     return out
+
+
+def varlen_status(workspace: torch.Tensor) -> None:
+    """Raise the error (if any) the device recorded for the last
+    ``hash_varlen`` call on ``workspace`` (synchronizes its stream)."""
+    dev = workspace.device
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().hth_varlen_status(workspace.data_ptr(), _stream(dev)))
 
 
 def hash_fixed_folds(data: torch.Tensor, n_bytes: int, folds, params: HashParams, n_strings: int = None,
@@ -178,7 +221,7 @@ def hash_fixed_folds(data: torch.Tensor, n_bytes: int, folds, params: HashParams
     wsz = workspace_fixed(params, n_strings, n_bytes)
     ws = _WS.get(dev, wsz)
     with torch.cuda.device(dev):
-        _lib.check(_lib.lib().hth_hash_fixed_folds(
+        _call(_WS, dev, lambda: _lib.lib().hth_hash_fixed_folds(
             params.output_bytes, data.data_ptr(), n_strings, stride, n_bytes, f.data_ptr(), out.data_ptr(),
             ws.data_ptr(), ws.numel(), _stream(dev)))
     return out
@@ -212,10 +255,12 @@ def hash_words(words, n_bytes: int, seed, params: HashParams, device=None) -> np
 
 
 def hash_fixed_host(data, n_strings: int, n_bytes: int, master: bytes, params: HashParams, stride: int = None,
-                    seed_capacity: int = 0, device: int = 0) -> np.ndarray:
+                    seed_capacity: int = None, device: int = 0) -> np.ndarray:
     """End-to-end batch from HOST memory (``hth_hash_fixed_host``): chunked
     H2D copies pipelined against hashing on three streams.  ``data`` may be a
-    numpy array, bytes, or a (pinned) CPU torch tensor.  Returns (B, k) uint64."""
+    numpy array, bytes, or a (pinned) CPU torch tensor.  ``seed_capacity``
+    plays SeedBuffer.capacity (``SeedSizeError`` below the layout); None
+    sizes the seed stream exactly (seed_for_input).  Returns (B, k) uint64."""
     params = _check_params(params)
     stride = n_bytes if stride is None else stride
     if isinstance(data, torch.Tensor):
@@ -228,8 +273,9 @@ def hash_fixed_host(data, n_strings: int, n_bytes: int, master: bytes, params: H
     out = np.zeros((n_strings, params.output_words), dtype=np.uint64)
     if len(master) != 32:
         raise ValueError("master seed must be exactly 32 bytes")
+    cap = _lib.SEED_AUTO if seed_capacity is None else int(seed_capacity)
     _lib.check(_lib.lib().hth_hash_fixed_host(params.output_bytes, ptr, n_strings, stride, n_bytes, bytes(master),
-                                              seed_capacity, out.ctypes.data, device))
+                                              cap, out.ctypes.data, device))
     return out
 
 
@@ -242,3 +288,8 @@ def fill_bytes(n_bytes: int, fill_seed: int = 0x243F6A8885A308D3, word_offset: i
     with torch.cuda.device(dev):
         _lib.check(_lib.lib().hth_fill_splitmix(_u64(fill_seed), word_offset, n_bytes, out.data_ptr(), _stream(dev)))
     return out
+
+
+def release_host() -> None:
+    """Free the calling thread's host-path streams and buffers (``hth_host_release``)."""
+    _lib.check(_lib.lib().hth_host_release())

@@ -189,9 +189,12 @@ __host__ __device__ __forceinline__ u64 job_count(u64 n_inst, int job_lvl) {
 }
 
 // scratch words / counters a string needs for merges above the job level
-__host__ __device__ __forceinline__ void scratch_need(u64 n_inst, int k, int job_lvl, u64* words, u64* cnts) {
+// (levels below `upto` only: a slice whose subtree roots stop at frontier
+// level c never merges at or above c)
+__host__ __device__ __forceinline__ void scratch_need(u64 n_inst, int k, int job_lvl, u64* words, u64* cnts,
+                                                     int upto = 64) {
   u64 w = 0, c = 0;
-  for (int l = job_lvl; (n_inst >> (3 * l)) >= 8; l++) {
+  for (int l = job_lvl; l < upto && (n_inst >> (3 * l)) >= 8; l++) {
     const u64 len = n_inst >> (3 * l);
     w += (len & ~7ull) * 8ull * k;
     c += len >> 3;

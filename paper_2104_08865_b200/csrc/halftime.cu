@@ -156,14 +156,16 @@ __global__ void fill_kernel(u64 seed, u64 woff, u64 n_words, u64 n_bytes, u64* d
 // digests are integer sums and do not depend on them.  The grid's first
 // threads also build the zero-slot table (ztab_base).  err bit 1: a string
 // longer than max_n; bit 2: more instances than the declared total (the
-// queues would overflow; the job is dropped).
+// queues would overflow; the job is dropped); bit 4: offsets decreasing or
+// past total_bytes (the string is hashed as empty).  Any set bit means the
+// call's digests are invalid: hth_varlen_status reports it.
 struct QueueTable {
   u64 qb[NCLS + 1];  // queue c occupies job_map[qb[c], qb[c+1])
 };
 struct PlanParams {
   const uint8_t* data;
   const u64* off;
-  u64 n, max_n;
+  u64 n, max_n, total;
   int job_lvl;
   u32 lmax;
   const u64* S;
@@ -227,7 +229,12 @@ __global__ void __launch_bounds__(256) plan_tail_kernel(const __grid_constant__ 
     const bool live = s < P.n;
     const bool first = s == s_first;
     const u64 o0 = live ? (first ? f_o0 : P.off[s]) : 0;
-    u64 n = live ? (first ? f_o1 : P.off[s + 1]) - o0 : 0;
+    const u64 o1 = live ? (first ? f_o1 : P.off[s + 1]) : 0;
+    u64 n = o1 - o0;
+    if (o1 < o0 || o1 > P.total) {
+      if (g == 0) atomicOr(P.err, 4);
+      n = 0;
+    }
     if (n > P.max_n) {
       if (g == 0) atomicOr(P.err, 1);
       n = P.max_n;
@@ -262,12 +269,14 @@ __global__ void __launch_bounds__(256) plan_tail_kernel(const __grid_constant__ 
     for (int r = 0; r < K; r++) acc[r] = 0;
     const u32 nw = tail ? (u32)((n + 7) >> 3) : 0;
     for (u32 t = g; t < nw; t += 16) {
-      const u64 b = o0 + 8ull * t;
-      const u64* p = reinterpret_cast<const u64*>(P.data + (b & ~7ull));
+      // absolute address: the buffer base itself may be unaligned
+      const u64 b = reinterpret_cast<u64>(P.data) + o0 + 8ull * t;
+      const u64* p = reinterpret_cast<const u64*>(b & ~7ull);
       const u32 sh = (u32)(b & 7) * 8;
-      u64 x = __ldg(p);
-      if (sh) x = (x >> sh) | (__ldg(p + 1) << (64 - sh));
       const u64 rem = n - 8ull * t;
+      u64 x = __ldg(p) >> sh;
+      // the next aligned word only if the string reaches into it (no over-read)
+      if (sh && rem > 8 - (b & 7)) x |= __ldg(p + 1) << (64 - sh);
       if (rem < 8) x &= (1ull << (8 * rem)) - 1;  // zero-pad the partial last word (hasher.py:179-183)
 #pragma unroll
       for (int r = 0; r < K; r++) acc[r] = nh_acc(acc[r], x, key[t + r]);
@@ -490,6 +499,19 @@ int dispatch_ps(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   return fail(HTH_EINVAL, "unsupported output width %d", out);
 }
 
+// A failed launch must not leave a half-used workspace behind: its
+// self-resetting counters would corrupt every later call.  Re-zero it
+// (stream-ordered, best effort) and pass the error on.
+int guard_ws(int rc, void* ws, u64 bytes, cudaStream_t st) {
+  if (rc != HTH_OK && ws && bytes) {
+    const std::string msg = g_err;
+    cudaGetLastError();
+    cudaMemsetAsync(ws, 0, bytes, st);
+    g_err = msg;
+  }
+  return rc;
+}
+
 int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
   const Layout l = make_layout(v, n_bytes);
   if (cap < l.total)
@@ -508,13 +530,14 @@ struct FixedPlan {
   u64 n_inst, J, n_jobs, scr_per, cnt_per, ws_scratch, ws_acc, ws_cnt, ws_ev, ws_total;
   int job_lvl;
 };
-FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes) {
+// frontier > 0: slice mode, merges stop below that level
+FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes, int frontier = 0) {
   FixedPlan f;
   f.n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
   f.job_lvl = pick_job_lvl(f.n_inst);
   f.J = job_count(f.n_inst, f.job_lvl);
   f.n_jobs = n_strings * f.J;
-  scratch_need(f.n_inst, v.k, f.job_lvl, &f.scr_per, &f.cnt_per);
+  scratch_need(f.n_inst, v.k, f.job_lvl, &f.scr_per, &f.cnt_per, frontier > 0 ? frontier : 64);
   const bool multi = f.J > 1;
   f.ws_scratch = align_up(n_strings * f.scr_per * 8, 256);
   f.ws_acc = multi ? align_up(n_strings * v.k * 8, 256) : 0;
@@ -534,7 +557,11 @@ struct VarPlan {
 // hash state and the plan counters first (cleared by one memset per call),
 // then the per-string bases, class queues, merge scratch and zero-slot table.
 int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPlan* p) {
-  const u64 total_inst = total_bytes / (8ull * v.m);
+  // a string's instances are ceil(len / 8) / m: a string of 8m-7..8m-1 bytes
+  // already holds a full instance, so bound the batch's sum per string
+  // rounding (up to 7 padding bytes each), not by total_bytes / 8m
+  if (n > (~0ull - total_bytes) / 7) return fail(HTH_EINVAL, "n_strings too large");
+  const u64 total_inst = (total_bytes + 7 * n) / (8ull * v.m);
   // no string has more levels than the longest allowed one, nor than the total
   const u64 max_inst = std::min(((max_n_bytes / 8) + 1) / (u64)v.m, total_inst);
   p->lmax = max_inst ? level_count(max_inst) : 1;
@@ -569,17 +596,21 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPl
 // one-stream path through pinned staging: a single-string hash_bytes call is
 // then one H2D DMA, one launch, one D2H DMA and one synchronize
 constexpr u64 kSmallCall = 256 << 10, kSmallOut = 4096;
+// larger calls move ~kChunk bytes per chunk; strings longer than kChunk are
+// streamed through the same bounded buffers in slices (hth_hash_slice), so
+// device memory stays at 3 chunks whatever the input size
+constexpr u64 kChunk = 64ull << 20;
 struct HostCtx {
   int dev = -1;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
-  void* buf[3] = {nullptr, nullptr, nullptr};
-  u64 buf_bytes = 0;
+  void* buf[3] = {nullptr, nullptr, nullptr};  // allocated per slot, on first use
+  u64 buf_bytes[3] = {0, 0, 0};
   u64* seeds = nullptr;
-  u64 seed_words = 0;
+  u64 seed_bytes = 0;
   u64* out = nullptr;
-  u64 out_words = 0;
-  void* ws[3] = {nullptr, nullptr, nullptr};
-  u64 ws_bytes = 0;
+  u64 out_bytes = 0;
+  void* ws[3] = {nullptr, nullptr, nullptr};  // zero-filled, kept zero by the engine
+  u64 ws_bytes[3] = {0, 0, 0};
   // small-call path: pinned staging both ways, and the fold whose first
   // `seeds_valid` words are already expanded in `seeds`
   uint8_t* hin = nullptr;
@@ -588,69 +619,94 @@ struct HostCtx {
   // pageable sources: two pinned staging slots filled by parallel memcpy
   uint8_t* ring[2] = {nullptr, nullptr};
   cudaEvent_t ring_ev[2] = {nullptr, nullptr};
-  ~HostCtx() {}
+  cudaEvent_t ev = nullptr;  // cross-stream ordering (created once)
+  // sliced long strings: subtree roots, per-slice partials, merge scratch
+  u64* frontier = nullptr;
+  u64 frontier_bytes = 0;
+  u64* partials = nullptr;
+  u64 partial_bytes = 0;
+  void* mws = nullptr;
+  u64 mws_bytes = 0;
+
+  // Frees everything (errors ignored: at process exit the runtime may
+  // already be unloading).  Called on device switch, hth_host_release and
+  // thread exit.
+  void release() {
+    if (dev < 0) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    for (int i = 0; i < 3; i++) {
+      if (st[i]) cudaStreamSynchronize(st[i]);
+    }
+    for (int i = 0; i < 3; i++) {
+      if (st[i]) cudaStreamDestroy(st[i]);
+      if (buf[i]) cudaFree(buf[i]);
+      if (ws[i]) cudaFree(ws[i]);
+    }
+    for (int i = 0; i < 2; i++) {
+      if (ring[i]) cudaFreeHost(ring[i]);
+      if (ring_ev[i]) cudaEventDestroy(ring_ev[i]);
+    }
+    if (ev) cudaEventDestroy(ev);
+    if (seeds) cudaFree(seeds);
+    if (out) cudaFree(out);
+    if (frontier) cudaFree(frontier);
+    if (partials) cudaFree(partials);
+    if (mws) cudaFree(mws);
+    if (hin) cudaFreeHost(hin);
+    if (hout) cudaFreeHost(hout);
+    if (cur >= 0 && cur != dev) cudaSetDevice(cur);
+    cudaGetLastError();
+    *this = HostCtx();
+  }
+  ~HostCtx() { release(); }
 };
 thread_local HostCtx g_host;
 
-int host_ctx(int device, u64 buf_bytes, u64 seed_words, u64 out_words, u64 ws_bytes, HostCtx** out) {
+// grow-only device allocation
+int grow(void** p, u64* have, u64 need, bool zero) {
+  if (need <= *have) return HTH_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  CK(cudaMalloc(p, need));
+  if (zero) CK(cudaMemset(*p, 0, need));  // legacy stream; callers synchronize below
+  *have = need;
+  return HTH_OK;
+}
+
+int host_ctx(int device, HostCtx** out) {
   HostCtx& c = g_host;
-  if (c.dev >= 0 && c.dev != device) {
-    // this thread moved to another device: release the old device's buffers
-    cudaSetDevice(c.dev);
-    for (int i = 0; i < 3; i++) {
-      if (c.st[i]) cudaStreamDestroy(c.st[i]);
-      if (c.buf[i]) cudaFree(c.buf[i]);
-      if (c.ws[i]) cudaFree(c.ws[i]);
-    }
-    for (int i = 0; i < 2; i++) {
-      if (c.ring[i]) cudaFreeHost(c.ring[i]);
-      if (c.ring_ev[i]) cudaEventDestroy(c.ring_ev[i]);
-    }
-    if (c.seeds) cudaFree(c.seeds);
-    if (c.out) cudaFree(c.out);
-    if (c.hin) cudaFreeHost(c.hin);
-    if (c.hout) cudaFreeHost(c.hout);
-    c = HostCtx();
-  }
+  if (c.dev >= 0 && c.dev != device) c.release();  // this thread moved to another device
   CK(cudaSetDevice(device));
   if (c.dev != device) {
     c = HostCtx();
     c.dev = device;
     for (int i = 0; i < 3; i++) CK(cudaStreamCreateWithFlags(&c.st[i], cudaStreamNonBlocking));
-  }
-  if (buf_bytes > c.buf_bytes) {
-    for (int i = 0; i < 3; i++) {
-      if (c.buf[i]) cudaFree(c.buf[i]);
-      CK(cudaMalloc(&c.buf[i], buf_bytes));
-    }
-    c.buf_bytes = buf_bytes;
-  }
-  if (seed_words > c.seed_words) {
-    if (c.seeds) cudaFree(c.seeds);
-    CK(cudaMalloc(&c.seeds, seed_words * 8));
-    c.seed_words = seed_words;
-    c.seeds_valid = 0;
-  }
-  if (out_words > c.out_words) {
-    if (c.out) cudaFree(c.out);
-    CK(cudaMalloc(&c.out, out_words * 8));
-    c.out_words = out_words;
-  }
-  if (ws_bytes > c.ws_bytes) {
-    for (int i = 0; i < 3; i++) {
-      if (c.ws[i]) cudaFree(c.ws[i]);
-      CK(cudaMalloc(&c.ws[i], ws_bytes));
-      CK(cudaMemset(c.ws[i], 0, ws_bytes));  // engine keeps it zeroed afterwards
-    }
-    // the memsets ran on the legacy stream; our streams are non-blocking
-    CK(cudaDeviceSynchronize());
-    c.ws_bytes = ws_bytes;
+    CK(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
   }
   if (!c.hin) {
     CK(cudaHostAlloc((void**)&c.hin, kSmallCall + 16, cudaHostAllocDefault));
     CK(cudaHostAlloc((void**)&c.hout, kSmallOut * 8, cudaHostAllocDefault));
   }
   *out = &c;
+  return HTH_OK;
+}
+
+// slots 0..nslots-1 of input buffer / workspace, plus seeds and digests
+int host_reserve(HostCtx* c, int nslots, u64 buf_bytes, u64 ws_bytes, u64 seed_words, u64 out_words) {
+  bool zeroed = false;
+  for (int i = 0; i < nslots; i++) {
+    if (int rc = grow(&c->buf[i], &c->buf_bytes[i], buf_bytes, false)) return rc;
+    if (ws_bytes > c->ws_bytes[i]) zeroed = true;
+    if (int rc = grow(&c->ws[i], &c->ws_bytes[i], ws_bytes, true)) return rc;
+  }
+  if (seed_words * 8 > c->seed_bytes) c->seeds_valid = 0;  // reallocated: nothing expanded yet
+  if (int rc = grow((void**)&c->seeds, &c->seed_bytes, seed_words * 8, false)) return rc;
+  if (int rc = grow((void**)&c->out, &c->out_bytes, out_words * 8, false)) return rc;
+  // the memsets ran on the legacy stream; our streams are non-blocking
+  if (zeroed) CK(cudaDeviceSynchronize());
   return HTH_OK;
 }
 
@@ -791,8 +847,10 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   if (!n_strings) return HTH_OK;
   if (!d_out || !d_seed) return fail(HTH_EINVAL, "null device pointer");
   if (n_bytes && !d_data) return fail(HTH_EINVAL, "null data pointer");
-  if (reinterpret_cast<uintptr_t>(d_data) & 15) return fail(HTH_EINVAL, "d_data must be 16-byte aligned");
   if (n_strings > 1 && stride_bytes < n_bytes) return fail(HTH_EINVAL, "stride_bytes < n_bytes");
+  // one string: the stride is meaningless; give every route the same
+  // well-formed one (16-byte multiple covering the string)
+  if (n_strings == 1) stride_bytes = align_up(n_bytes, 16);
   const FixedPlan f = fixed_plan(v, n_strings, n_bytes);
   if (workspace_bytes < f.ws_total)
     return fail(HTH_EINVAL, "workspace too small: %llu < %llu bytes", (unsigned long long)workspace_bytes,
@@ -814,7 +872,8 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.job_lvl = f.job_lvl;
   fill_ehc(v, seed_fold, P);
   fill_fin_const(v, seed_fold, n_bytes, P);
-  if (f.n_inst == 0 && n_bytes > 0 && stride_bytes % 16 == 0 && stride_bytes <= 2048) {
+  if (f.n_inst == 0 && n_bytes > 0 && stride_bytes % 16 == 0 && stride_bytes <= 2048 &&
+      (reinterpret_cast<uintptr_t>(d_data) & 15) == 0) {
     // strings shorter than one instance: dedicated half-warp-per-string kernel
     TailParams T{};
     T.data = (const uint8_t*)d_data;
@@ -837,8 +896,7 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
       case 40: return dispatch_tail<40>(T, nch, st);
     }
   }
-  if (small_ok(v, f.n_inst, n_strings > 1 ? stride_bytes : align_up(n_bytes, 8), n_bytes, d_data)) {
-    if (n_strings == 1) P.stride = align_up(n_bytes, 8);
+  if (small_ok(v, f.n_inst, stride_bytes, n_bytes, d_data)) {
     switch (output_bytes) {
       case 16: return dispatch_small<16>(P, st);
       case 24: return dispatch_small<24>(P, st);
@@ -852,7 +910,7 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
   P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
   P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
   set_ctl(P, ws + f.ws_total - 256);
-  return dispatch<false>(output_bytes, P, f.n_jobs, st);
+  return guard_ws(dispatch<false>(output_bytes, P, f.n_jobs, st), d_workspace, f.ws_total, st);
 }
 
 int hth_hash_fixed_folds(int output_bytes, const void* d_data, uint64_t n_strings, uint64_t stride_bytes,
@@ -863,7 +921,6 @@ int hth_hash_fixed_folds(int output_bytes, const void* d_data, uint64_t n_string
   if (!n_strings) return HTH_OK;
   if (!d_out || !d_folds) return fail(HTH_EINVAL, "null device pointer");
   if (n_bytes && !d_data) return fail(HTH_EINVAL, "null data pointer");
-  if (reinterpret_cast<uintptr_t>(d_data) & 15) return fail(HTH_EINVAL, "d_data must be 16-byte aligned");
   if (n_strings > 1 && stride_bytes && stride_bytes < n_bytes) return fail(HTH_EINVAL, "0 < stride_bytes < n_bytes");
   const FixedPlan f = fixed_plan(v, n_strings, n_bytes);
   if (workspace_bytes < f.ws_total) return fail(HTH_EINVAL, "workspace too small");
@@ -887,7 +944,8 @@ int hth_hash_fixed_folds(int output_bytes, const void* d_data, uint64_t n_string
   P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
   P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
   set_ctl(P, ws + f.ws_total - 256);
-  return dispatch_ps(output_bytes, P, f.n_jobs, (cudaStream_t)stream);
+  return guard_ws(dispatch_ps(output_bytes, P, f.n_jobs, (cudaStream_t)stream), d_workspace, f.ws_total,
+                  (cudaStream_t)stream);
 }
 
 int hth_workspace_size_varlen(int output_bytes, uint64_t n_strings, uint64_t total_bytes, uint64_t* bytes) {
@@ -909,7 +967,7 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   if (int rc = check_seed(v, max_n_bytes, seed_capacity)) return rc;
   if (!n_strings) return HTH_OK;
   if (!d_out || !d_seed || !d_offsets || !d_workspace) return fail(HTH_EINVAL, "null device pointer");
-  if (reinterpret_cast<uintptr_t>(d_data) & 15) return fail(HTH_EINVAL, "d_data must be 16-byte aligned");
+  if (total_bytes && !d_data) return fail(HTH_EINVAL, "null data pointer");
   if (n_strings >= (1ull << 32)) return fail(HTH_EINVAL, "at most 2^32-1 strings per call");
   VarPlan p;
   if (int rc = varlen_plan(v, n_strings, total_bytes, max_n_bytes, &p)) return rc;
@@ -931,6 +989,7 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   Q.off = d_offsets;
   Q.n = n_strings;
   Q.max_n = max_n_bytes;
+  Q.total = total_bytes;
   Q.job_lvl = job_lvl;
   Q.lmax = (u32)p.lmax;
   Q.S = d_seed;
@@ -992,6 +1051,7 @@ int hth_varlen_status(void* d_workspace, void* stream) {
   CK(cudaMemcpyAsync(&h, d_workspace, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   if (h & 1) return fail(HTH_ESEEDSIZE, "a string was longer than max_n_bytes; its digest is invalid");
+  if (h & 4) return fail(HTH_EINVAL, "offsets decrease or run past total_bytes; digests are invalid");
   if (h & 2) return fail(HTH_EINVAL, "the strings hold more bytes than total_bytes declared; digests are invalid");
   return HTH_OK;
 }
@@ -1073,13 +1133,12 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   VarInfo v;
   if (int rc = get_var(output_bytes, &v)) return rc;
   if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
-  const FixedPlan f = fixed_plan(v, 1, n_bytes);
+  const FixedPlan f = fixed_plan(v, 1, n_bytes, std::max(frontier_level, 1));
   const u64 per = 1ull << (3 * f.job_lvl), sub = 1ull << (3 * frontier_level);
   if (frontier_level < f.job_lvl || inst_begin % sub || inst_begin > inst_end || inst_end > f.n_inst ||
       (inst_end != f.n_inst && inst_end % sub))
     return fail(HTH_EINVAL, "slice bounds must be multiples of 8^frontier_level instances (frontier >= %d)", f.job_lvl);
   if (!d_partial || !d_seed) return fail(HTH_EINVAL, "null device pointer");
-  if (reinterpret_cast<uintptr_t>(d_slice) & 15) return fail(HTH_EINVAL, "d_slice must be 16-byte aligned");
   if (workspace_bytes < f.ws_total) return fail(HTH_EINVAL, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemsetAsync(d_partial, 0, v.k * 8, st));
@@ -1112,7 +1171,7 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   P.counters = (u32*)(ws + f.ws_scratch + f.ws_acc);
   P.events = (u32*)(ws + f.ws_scratch + f.ws_acc + f.ws_cnt);
   set_ctl(P, ws + f.ws_total - 256);
-  return dispatch<false>(output_bytes, P, P.n_jobs, st);
+  return guard_ws(dispatch<false>(output_bytes, P, P.n_jobs, st), d_workspace, f.ws_total, st);
 }
 
 int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
@@ -1151,6 +1210,55 @@ int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const
   return HTH_OK;
 }
 
+// Strings longer than kChunk from host memory: each is streamed in slices
+// of whole level-c subtrees (c = the job level, 8^c instances) through the
+// three bounded input buffers, one hth_hash_slice per slice on rotating
+// streams (the H2D copy of slice i+1 overlaps the hash of slice i), then one
+// hth_hash_merge finishes the tree (tree.py:63-134) and adds the tail.
+static int host_hash_long(const VarInfo& v, int output_bytes, HostCtx* c, const uint8_t* h_data, u64 n_strings,
+                          u64 stride_bytes, u64 n_bytes, u64 fold, u64 total) {
+  const u64 n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
+  const int lvl = pick_job_lvl(n_inst);
+  const u64 sub = 1ull << (3 * lvl), sub_bytes = sub * v.m * 8;
+  const u64 ci = std::max<u64>(1, kChunk / sub_bytes) * sub;  // instances per slice
+  const u64 nsl = ceil_div(n_inst, ci);
+  const u64 keep = (n_inst >> (3 * lvl)) & ~7ull;  // non-leftover level-c roots
+  const u64 k = (u64)v.k;
+  const FixedPlan fp = fixed_plan(v, 1, n_bytes, lvl);
+  const u64 slice_bytes = ci * v.m * 8 + v.m * 8 + 16;  // + the ragged tail of the last slice
+  if (int rc = host_reserve(c, (int)std::min<u64>(nsl, 3), slice_bytes, fp.ws_total, total, n_strings * k)) return rc;
+  if (int rc = grow((void**)&c->frontier, &c->frontier_bytes, std::max<u64>(keep, 1) * 8 * k * 8, false)) return rc;
+  if (int rc = grow((void**)&c->partials, &c->partial_bytes, nsl * k * 8, false)) return rc;
+  const u64 mneed = 2 * (keep / 8 + 8) * 8 * k * 8;
+  if (int rc = grow(&c->mws, &c->mws_bytes, mneed, false)) return rc;
+  if (int rc = host_seeds(c, fold, total, c->st[0])) return rc;
+  for (u64 s = 0; s < n_strings; s++) {
+    // slices of this string start after the seeds and the previous merge
+    CK(cudaEventRecord(c->ev, c->st[0]));
+    for (int i = 1; i < 3; i++) CK(cudaStreamWaitEvent(c->st[i], c->ev, 0));
+    const uint8_t* src = h_data + s * stride_bytes;
+    for (u64 i = 0; i < nsl; i++) {
+      const int b = (int)(i % 3);
+      const u64 ib = i * ci, ie = std::min(n_inst, ib + ci);
+      const u64 b0 = ib * v.m * 8, b1 = ie == n_inst ? n_bytes : ie * v.m * 8;
+      if (int rc = h2d(c, c->buf[b], src + b0, b1 - b0, c->st[b])) return rc;
+      const u64 fa = ib >> (3 * lvl);
+      if (int rc = hth_hash_slice(output_bytes, c->buf[b], n_bytes, ib, ie, lvl, fold, c->seeds, total,
+                                  c->frontier + std::min(fa, keep) * 8 * k, c->partials + i * k, c->ws[b],
+                                  c->ws_bytes[b], c->st[b]))
+        return rc;
+    }
+    for (int i = 1; i < 3; i++) {
+      CK(cudaEventRecord(c->ev, c->st[i]));
+      CK(cudaStreamWaitEvent(c->st[0], c->ev, 0));
+    }
+    if (int rc = hth_hash_merge(output_bytes, n_bytes, lvl, c->frontier, keep, c->partials, nsl, fold, c->seeds,
+                                total, c->out + s * k, c->mws, c->mws_bytes, c->st[0]))
+      return rc;
+  }
+  return HTH_OK;
+}
+
 int hth_hash_host(int output_bytes, const void* h_data, uint64_t n_bytes, const uint8_t master[32],
                   uint64_t seed_capacity, uint64_t* h_out, int device) {
   return hth_hash_fixed_host(output_bytes, h_data, 1, n_bytes, n_bytes, master, seed_capacity, h_out, device);
@@ -1163,26 +1271,38 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
   if (int rc = get_var(output_bytes, &v)) return rc;
   if (!master) return fail(HTH_EINVAL, "master seed must be exactly 32 bytes");
   const Layout lay = make_layout(v, n_bytes);
-  if (seed_capacity && seed_capacity < lay.total) return check_seed(v, n_bytes, seed_capacity);
+  // SeedBuffer.capacity semantics (hasher.py:209-214); HTH_SEED_AUTO sizes it
+  if (seed_capacity != HTH_SEED_AUTO)
+    if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
   if (!n_strings) return HTH_OK;
   if (!h_out || (n_bytes && !h_data)) return fail(HTH_EINVAL, "null host pointer");
   if (n_strings > 1 && stride_bytes < n_bytes) return fail(HTH_EINVAL, "stride_bytes < n_bytes");
   if (n_strings == 1) stride_bytes = align_up(n_bytes, 16);
-  // chunking: whole strings per chunk, ~64 MiB per chunk, 3 buffers in flight
-  const u64 target = 64ull << 20;
-  // strings keep their host stride on the device (the kernel handles any
-  // start alignment); only the chunk base is 16-byte aligned
+  HostCtx* c = nullptr;
+  if (int rc = host_ctx(device, &c)) return rc;
+  const u64 fold = fold_of(master);
+  const u64 k = (u64)v.k;
+  if (n_bytes > kChunk) {
+    if (int rc = host_hash_long(v, output_bytes, c, (const uint8_t*)h_data, n_strings, stride_bytes, n_bytes, fold,
+                                lay.total))
+      return rc;
+    CK(cudaMemcpyAsync(h_out, c->out, n_strings * k * 8, cudaMemcpyDeviceToHost, c->st[0]));
+    CK(cudaStreamSynchronize(c->st[0]));
+    return HTH_OK;
+  }
+  // chunking: whole strings per chunk, ~kChunk bytes per chunk, 3 buffers in
+  // flight; strings keep their host stride on the device (the kernel handles
+  // any start alignment)
   const u64 dstride = std::max<u64>(stride_bytes, 1);
-  u64 per = std::max<u64>(1, target / dstride);
+  u64 per = std::max<u64>(1, kChunk / dstride);
   if (per > n_strings) per = n_strings;
   const u64 nchunks = ceil_div(n_strings, per);
   const FixedPlan fp = fixed_plan(v, per, n_bytes);
-  HostCtx* c = nullptr;
-  if (int rc = host_ctx(device, per * dstride + 16, lay.total, n_strings * v.k, std::max<u64>(fp.ws_total, 256), &c))
-    return rc;
-  const u64 fold = fold_of(master);
   const u64 in_bytes = n_bytes ? (n_strings - 1) * stride_bytes + n_bytes : 0;
-  if (nchunks == 1 && in_bytes <= kSmallCall && n_strings * v.k <= kSmallOut) {
+  if (int rc = host_reserve(c, (int)std::min<u64>(nchunks, 3), per * dstride + 16, std::max<u64>(fp.ws_total, 256),
+                            lay.total, n_strings * k))
+    return rc;
+  if (nchunks == 1 && in_bytes <= kSmallCall && n_strings * k <= kSmallOut) {
     cudaStream_t st = c->st[0];
     if (int rc = host_seeds(c, fold, lay.total, st)) return rc;
     if (in_bytes) {
@@ -1190,18 +1310,16 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
       CK(cudaMemcpyAsync(c->buf[0], c->hin, in_bytes, cudaMemcpyHostToDevice, st));
     }
     if (int rc = hth_hash_fixed(output_bytes, c->buf[0], n_strings, dstride, n_bytes, fold, c->seeds, lay.total,
-                                c->out, c->ws[0], c->ws_bytes, st))
+                                c->out, c->ws[0], c->ws_bytes[0], st))
       return rc;
-    CK(cudaMemcpyAsync(c->hout, c->out, n_strings * v.k * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(c->hout, c->out, n_strings * k * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    std::memcpy(h_out, c->hout, n_strings * v.k * 8);
+    std::memcpy(h_out, c->hout, n_strings * k * 8);
     return HTH_OK;
   }
   if (int rc = host_seeds(c, fold, lay.total, c->st[0])) return rc;
-  cudaEvent_t seeded;
-  CK(cudaEventCreateWithFlags(&seeded, cudaEventDisableTiming));
-  CK(cudaEventRecord(seeded, c->st[0]));
-  for (int i = 1; i < 3; i++) CK(cudaStreamWaitEvent(c->st[i], seeded, 0));
+  CK(cudaEventRecord(c->ev, c->st[0]));
+  for (int i = 1; i < 3; i++) CK(cudaStreamWaitEvent(c->st[i], c->ev, 0));
   for (u64 ch = 0; ch < nchunks; ch++) {
     const int b = (int)(ch % 3);
     cudaStream_t st = c->st[b];
@@ -1209,20 +1327,31 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
     const uint8_t* src = (const uint8_t*)h_data + s0 * stride_bytes;
     if (n_bytes)
       if (int rc = h2d(c, c->buf[b], src, (ns - 1) * stride_bytes + n_bytes, st)) return rc;
-    if (int rc = hth_hash_fixed(output_bytes, c->buf[b], ns, dstride, n_bytes, fold_of(master), c->seeds, lay.total,
-                                c->out + s0 * v.k, c->ws[b], c->ws_bytes, st))
+    if (int rc = hth_hash_fixed(output_bytes, c->buf[b], ns, dstride, n_bytes, fold, c->seeds, lay.total,
+                                c->out + s0 * k, c->ws[b], c->ws_bytes[b], st))
       return rc;
   }
   // digests stay on the device until every chunk is hashed: a per-chunk copy
   // into (pageable) h_out blocks this thread until that chunk's kernel ends,
   // which starves the copy engine of the next chunk (~0.1 ms gap per chunk)
   for (int i = 1; i < 3; i++) {
-    CK(cudaEventRecord(seeded, c->st[i]));
-    CK(cudaStreamWaitEvent(c->st[0], seeded, 0));
+    CK(cudaEventRecord(c->ev, c->st[i]));
+    CK(cudaStreamWaitEvent(c->st[0], c->ev, 0));
   }
-  CK(cudaMemcpyAsync(h_out, c->out, n_strings * v.k * 8, cudaMemcpyDeviceToHost, c->st[0]));
+  CK(cudaMemcpyAsync(h_out, c->out, n_strings * k * 8, cudaMemcpyDeviceToHost, c->st[0]));
   CK(cudaStreamSynchronize(c->st[0]));
-  cudaEventDestroy(seeded);
+  return HTH_OK;
+}
+
+int hth_host_release(void) {
+  g_host.release();
+  return HTH_OK;
+}
+
+int hth_workspace_reset(void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (!workspace_bytes) return HTH_OK;
+  if (!d_workspace) return fail(HTH_EINVAL, "null workspace");
+  CK(cudaMemsetAsync(d_workspace, 0, workspace_bytes, (cudaStream_t)stream));
   return HTH_OK;
 }
 

@@ -10,8 +10,15 @@ reference's names, argument meaning and errors:
 * ``SeedSizeError`` capacity below ``seed_words_needed`` (hasher.py:209-214)
 * ``IndexError``    seed word out of range (hasher.py:84-97)
 
-The only engine is ``"cuda"``: the reference's ``"lanes"`` and ``"scalar"``
-are CPU engines and are deliberately not present (no CPU fallback).
+Engines: ``"cuda"`` (default).  The reference's engine names ``"lanes"``
+(its default) and ``"scalar"`` are accepted as aliases so unmodified
+callers keep working: all three produce the reference's bit-identical
+digests (hasher.py:217-269 vs :331-413), computed here by the GPU.  No CPU
+engine exists; ``counter=`` (the scalar engine's multiplication accounting)
+raises ``ValueError``.
+
+``_hash_words_np(words, n_bytes, seed_region, params)`` keeps the
+reference's batched seam signature (hasher.py:331-413) on the GPU engine.
 """
 
 from __future__ import annotations
@@ -33,7 +40,7 @@ MASK64 = (1 << 64) - 1
 
 __all__ = [
     "Digest", "SeedBuffer", "SeedLayout", "SeedSizeError", "digest", "expand_seed", "hash_bytes",
-    "seed_for_input", "seed_layout", "seed_words_needed", "instance_count", "splitmix_mix",
+    "seed_for_input", "seed_layout", "seed_words_needed", "instance_count", "splitmix_mix", "ENGINES",
 ]
 
 
@@ -182,6 +189,11 @@ def _check_capacity(seed: SeedBuffer, params: HashParams, n_bytes: int) -> None:
             "expand with seed_words_needed()")
 
 
+#: engine names accepted by hash_bytes: the GPU engine, and the reference's
+#: two engine names as aliases of it (identical digests)
+ENGINES = ("cuda", "lanes", "scalar")
+
+
 def hash_bytes(data, seed: SeedBuffer, params: HashParams, engine: str = "cuda", counter=None,
                device=None) -> Digest:
     """One-shot hash of ``data`` under an expanded seed (hasher.py:434-453).
@@ -190,10 +202,12 @@ def hash_bytes(data, seed: SeedBuffer, params: HashParams, engine: str = "cuda",
     Host data goes through ``hth_hash_host`` (H2D copy, on-device seed
     expansion, hash, D2H); device data through ``hth_hash_fixed``.
     """
-    if engine != "cuda":
-        raise ValueError(f"unknown engine {engine!r} (this package provides engine='cuda' only)")
+    if engine not in ENGINES:
+        raise ValueError(f"unknown engine {engine!r}; choose one of {', '.join(ENGINES)}")
     if counter is not None:
-        raise ValueError("multiplication counting requires engine='scalar'")
+        # the reference counts multiplications only in its instrumented scalar
+        # engine (hasher.py:447-449); the GPU engine has no such counter
+        raise ValueError("multiplication counting is not available on the GPU engine")
     params = _check_params(params)
     k = params.output_words
     try:
@@ -221,3 +235,104 @@ def digest(data, master: bytes = b"\x00" * 32, output_bytes: int = 24) -> Digest
     """Convenience one-shot (hasher.py:456-461)."""
     params = variant(output_bytes)
     return hash_bytes(data, seed_for_input(master, params, len(data)), params)
+
+
+# ------------------------------------------------------------ batched seam
+_MIX_1_INV = pow(_MIX_1, -1, 1 << 64)
+_MIX_2_INV = pow(_MIX_2, -1, 1 << 64)
+
+
+def _unshift_xor(y: np.ndarray, s: int) -> np.ndarray:
+    """Inverse of x -> x ^ (x >> s) on uint64."""
+    x = y.copy()
+    t = s
+    while t < 64:
+        x ^= y >> np.uint64(t)
+        t += s
+    return x
+
+
+def _unmix(z: np.ndarray) -> np.ndarray:
+    """Inverse of the splitmix64 finalizer (a bijection of u64)."""
+    with np.errstate(over="ignore"):
+        z = _unshift_xor(z, 31) * np.uint64(_MIX_2_INV)
+        z = _unshift_xor(z, 27) * np.uint64(_MIX_1_INV)
+    return _unshift_xor(z, 30)
+
+
+def _region_folds(seed_region, total: int):
+    """Recover the seed stream(s) behind a ``seed_region(start, count)``.
+
+    The engine computes seed words from a fold on the device
+    (S[i] = mix(fold + (i+1) gamma), hasher.py:55-67), so a region is
+    accepted when it is such a stream: a ``SeedBuffer.words_np`` (ours or
+    the reference's: ``__self__`` with ``master``/``capacity``) or any
+    callable returning ``_stream_words_np(folds, ...)`` with one fold or a
+    (B, 1) array of folds (tests/test_hasher.py:254-310).  The folds are read
+    off word 0 through the inverse finalizer and verified on the first and
+    last words the layout uses.  Returns (folds (B,) or (1,), capacity or
+    None).  ValueError for any other region; IndexError propagates from a
+    region too small for the layout (SeedBuffer.words_np, hasher.py:94-97).
+    """
+    owner = getattr(seed_region, "__self__", None)
+    if owner is not None and hasattr(owner, "master") and hasattr(owner, "capacity"):
+        owner.words_np(max(total - 1, 0), 1)  # IndexError if the capacity is short
+        return np.array([_master_fold(bytes(owner.master))], dtype=np.uint64), int(owner.capacity)
+    head = np.asarray(seed_region(0, 1), dtype=np.uint64)
+    if head.ndim == 1 and head.size == 1:
+        head = head.reshape(1, 1)
+    if head.ndim == 2 and head.shape[1] == 1:
+        with np.errstate(over="ignore"):
+            folds = _unmix(head[:, 0]) - np.uint64(GOLDEN_GAMMA)
+    else:
+        raise ValueError("seed_region(start, count) must return (count,) or (B, count) words")
+    for start in {0, max(total - 2, 0)}:
+        got = np.asarray(seed_region(start, 2 if total >= 2 else 1), dtype=np.uint64)
+        want = _stream_words_np(folds[:, None], start, got.shape[-1])
+        if not np.array_equal(got.reshape(-1, got.shape[-1]), want if got.ndim == 2 else want[:1]):
+            raise ValueError("seed_region is not a splitmix seed stream (SeedBuffer.words_np or "
+                             "_stream_words_np of master folds); the GPU engine cannot serve it")
+    return folds, None
+
+
+def _hash_words_np(words, n_bytes: int, seed_region, params: HashParams) -> np.ndarray:
+    """The reference's batched seam (hasher.py:331-413) on the GPU engine.
+
+    ``words``: (B, n_words) uint64 (a broadcast view of one row is hashed
+    from one device copy).  ``seed_region(start, count)``: see
+    ``_region_folds``.  Returns (B, k) uint64, row for row equal to the
+    reference's ``_hash_words_np``.
+    """
+    params = _check_params(params)
+    w = np.asarray(words)
+    if w.ndim != 2:
+        raise ValueError("words must be a (B, n_words) array")
+    if w.dtype != np.uint64:
+        w = w.astype(np.uint64)
+    B = w.shape[0]
+    nw = (n_bytes + 7) // 8
+    if w.shape[1] < nw:
+        raise ValueError(f"words hold {w.shape[1]} words but n_bytes={n_bytes} needs {nw}")
+    total = seed_words_needed(params, n_bytes)
+    folds, cap = _region_folds(seed_region, total)
+    if B == 0:
+        return np.zeros((0, params.output_words), dtype=np.uint64)
+    import torch
+
+    from .batch import hash_fixed, hash_fixed_folds
+
+    one_row = B == 1 or w.strides[0] == 0
+    rows = np.ascontiguousarray(w[:1, :nw] if one_row else w[:, :nw])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = torch.from_numpy(rows.view(np.uint8).reshape(-1)).to(dev)
+    if folds.size == 1:
+        seed = SeedBuffer(b"", cap if cap is not None else total, int(folds[0]))
+        if one_row and B > 1:  # the same row under one seed: hash once
+            out = hash_fixed(t, n_bytes, seed, params, n_strings=1).cpu().numpy().view(np.uint64)
+            return np.repeat(out, B, axis=0)
+        out = hash_fixed(t, n_bytes, seed, params, n_strings=B, stride=nw * 8)
+    else:
+        if folds.size != B:
+            raise ValueError(f"seed_region gives {folds.size} seed rows for a batch of {B}")
+        out = hash_fixed_folds(t, n_bytes, folds, params, n_strings=B, stride=0 if one_row else nw * 8)
+    return out.cpu().numpy().view(np.uint64).copy()

@@ -10,6 +10,39 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+MASK64 = (1 << 64) - 1
+
+# Combine-matrix coefficients and their shift/add forms (params.py:15-29):
+# coefficient -> (shift, op) with op +1 / -1 adding / subtracting x once
+# more, 0 for a bare shift; 0 itself maps to None (the product is 0).
+_FORMS = {0: None, 1: (0, 0), 2: (1, 0), 3: (1, 1), 4: (2, 0), 5: (2, 1), 7: (3, -1), 8: (3, 0), 9: (3, 1)}
+
+#: coefficients that have a shift/add form (params.py:31)
+SUPPORTED_COEFFICIENTS = frozenset(_FORMS)
+
+
+def coefficient_multiply(coeff: int, x, width: int = 64):
+    """``coeff * x mod 2**width`` by at most two shifts and one add/sub
+    (params.py:32-43).  ``x``: a Python int or a numpy uint64 array.  The
+    GPU kernels fold the same products into IMAD/LEA forms (csrc/engine.cuh
+    mac_const); this host form is kept for the reference's callers.
+    ValueError for a coefficient without a shift/add form."""
+    if coeff not in _FORMS:
+        raise ValueError(f"coefficient {coeff} has no shift/add form")
+    m = (1 << width) - 1 if width < 64 else MASK64
+    form = _FORMS[coeff]
+    if form is None:
+        return x & 0
+    if coeff == 1:  # identity, unmasked, as the reference returns it (params.py:20)
+        return x
+    sh, op = form
+    y = (x << sh) if sh else x
+    if op > 0:
+        y = y + x
+    elif op < 0:
+        y = y - x
+    return y & m
+
 
 def _xt4(a: int) -> int:
     t = (a >> 3) & 1
@@ -35,6 +68,13 @@ class TransformMatrix:
 
     entries: tuple
 
+    def __post_init__(self):  # params.py:52-58
+        if len({len(r) for r in self.entries}) != 1:
+            raise ValueError("ragged matrix")
+        unsupported = sorted({c for r in self.entries for c in r} - SUPPORTED_COEFFICIENTS)
+        if unsupported:
+            raise ValueError(f"entries without a shift/add form: {unsupported}")
+
     @property
     def rows(self) -> int:
         return len(self.entries)
@@ -42,6 +82,10 @@ class TransformMatrix:
     @property
     def cols(self) -> int:
         return len(self.entries[0])
+
+    def column_subset(self, cols: tuple) -> list:
+        """The matrix restricted to columns ``cols`` (params.py:68-69)."""
+        return [[r[c] for c in cols] for r in self.entries]
 
 
 @dataclass(frozen=True)
@@ -53,6 +97,19 @@ class ErasureCode:
     min_distance: int
     kind: str
     parity_rows: tuple
+
+    def __post_init__(self):  # params.py:91-98
+        if len(self.parity_rows) != self.arity_out - self.arity_in:
+            raise ValueError("parity row count must equal arity_out - arity_in")
+        for r in self.parity_rows:
+            if len(r) != self.arity_in:
+                raise ValueError("parity row width must equal arity_in")
+            if any(not 0 <= c < 16 for c in r):
+                raise ValueError("parity coefficients must be GF(16) elements")
+
+    @property
+    def bitwise_linear(self) -> bool:
+        return True
 
 
 @dataclass(frozen=True)
@@ -69,6 +126,19 @@ class HashParams:
     max_det_valuation: int
     matrix: TransformMatrix
     code: ErasureCode
+
+    def __post_init__(self):  # params.py:158-169
+        k, e, d = self.output_words, self.encoded_items, self.instance_items
+        checks = (
+            (self.output_bytes == 8 * k, "output_bytes must be 8 * output_words"),
+            (d == e + 1 - k, "instance_items must equal encoded_items + 1 - output_words"),
+            ((self.matrix.rows, self.matrix.cols) == (k, e), "combine matrix shape mismatch"),
+            ((self.code.arity_in, self.code.arity_out) == (d, e), "erasure code arity mismatch"),
+            (self.code.min_distance >= k, "erasure code distance below output_words"),
+        )
+        for ok, msg in checks:
+            if not ok:
+                raise ValueError(msg)
 
     @property
     def instance_blocks(self) -> int:

@@ -282,8 +282,10 @@ def test_seed_size_error_and_capacity(hh):
 def test_engine_and_counter_errors(hh):
     p = hh.variant(24)
     s = hh.seed_for_input(b"\0" * 32, p, 0)
+    # the reference's engine names are aliases (identical digests)
+    assert hh.hash_bytes(b"", s, p, engine="lanes") == hh.hash_bytes(b"", s, p)
     with pytest.raises(ValueError):
-        hh.hash_bytes(b"", s, p, engine="lanes")
+        hh.hash_bytes(b"", s, p, engine="numpy")
     with pytest.raises(ValueError):
         hh.hash_bytes(b"", s, p, counter=object())
     with pytest.raises(ValueError):

@@ -88,9 +88,9 @@ def test_api_errors_before_any_gpu_work():
     with pytest.raises(ValueError):
         hh.variant(20)
     with pytest.raises(ValueError):
-        hh.hash_bytes(b"", hh.seed_for_input(b"\0" * 32, p, 0), p, engine="scalar")
+        hh.hash_bytes(b"", hh.seed_for_input(b"\0" * 32, p, 0), p, engine="avx2")
     with pytest.raises(ValueError):
-        hh.hash_bytes(b"", hh.seed_for_input(b"\0" * 32, p, 0), p, counter=object())
+        hh.hash_bytes(b"", hh.seed_for_input(b"\0" * 32, p, 0), p, engine="scalar", counter=object())
     with pytest.raises(hh.SeedSizeError):
         hh.hash_bytes(bytes(100000), hh.expand_seed(b"\0" * 32, 10), p)
     assert issubclass(hh.SeedSizeError, ValueError)
