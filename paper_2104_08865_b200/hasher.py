@@ -322,7 +322,7 @@ def _hash_words_np(words, n_bytes: int, seed_region, params: HashParams) -> np.n
     from .batch import hash_fixed, hash_fixed_folds
 
     one_row = B == 1 or w.strides[0] == 0
-    rows = np.ascontiguousarray(w[:1, :nw] if one_row else w[:, :nw])
+    rows = np.array(w[:1, :nw] if one_row else w[:, :nw], dtype=np.uint64, order="C")  # own, writable copy
     dev = torch.device("cuda", torch.cuda.current_device())
     t = torch.from_numpy(rows.view(np.uint8).reshape(-1)).to(dev)
     if folds.size == 1:
