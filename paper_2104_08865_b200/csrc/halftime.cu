@@ -13,15 +13,15 @@
 
 
 #include "../../include/halftime_b200.h"
-#include "hash_kernel.cuh"
-#include "small_kernel.cuh"
-#include "tail_kernel.cuh"
-#include "merge_kernel.cuh"
+#include "engine_api.cuh"
 
 using namespace hth;
 
 namespace {
 
+// runtime helpers shared with the per-variant kernel units (rt.cuh)
+}  // namespace
+namespace hth {
 thread_local std::string g_err;
 
 int fail(int code, const char* fmt, ...) {
@@ -36,12 +36,45 @@ int fail(int code, const char* fmt, ...) {
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(e == cudaErrorMemoryAllocation ? HTH_ENOMEM : HTH_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
-#define CK(call)                                      \
-  do {                                                \
-    cudaError_t e_ = (call);                          \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-  } while (0)
+int sm_count(int dev) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev];
+}
 
+// Resident CTAs per SM of `kern` at (tpb, smem) on the current device; the
+// dynamic shared-memory limit is raised once per (kernel, device, smem) and
+// the answer cached, keeping the per-call host path to the launch itself.
+int occupancy(const void* kern, int tpb, size_t smem, int* dev_out, int* occ_out) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> limit;  // the attribute is per kernel: only raise it
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  *dev_out = dev;
+  const auto key = std::make_tuple(kern, dev, smem, tpb);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *occ_out = it->second;
+    return HTH_OK;
+  }
+  size_t& lim = limit[std::make_pair(kern, dev)];
+  if (smem > lim) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    lim = smem;
+  }
+  int o = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, tpb, smem));
+  cache[key] = *occ_out = std::max(o, 1);
+  return HTH_OK;
+}
+
+}  // namespace hth
+namespace {
 u64 align_up(u64 x, u64 a) { return (x + a - 1) / a * a; }
 
 struct Layout {
@@ -145,324 +178,6 @@ __global__ void fill_kernel(u64 seed, u64 woff, u64 n_words, u64 n_bytes, u64* d
   }
 }
 
-// Varlen plan + short strings (one kernel).  One half-warp per string: lane
-// 0 plans it -- a string of >= 1 instance appends its jobs to the queue of
-// their size class (min(instances, 64)), which the hash kernel claims largest
-// class first (LPT scheduling with dynamic claiming) -- and a string shorter
-// than one instance is hashed right here by its 16 lanes:
-//   D_r = NH(n, S[F_r]) + sum_i NH(W_i, S[R + r + i])   (hasher.py:400-412)
-// with the Toeplitz keys staged in shared memory.  Queue order inside a class
-// and the scratch/counter bases of multi-job strings come from atomics:
-// digests are integer sums and do not depend on them.  The grid's first
-// threads also build the zero-slot table (ztab_base).  err bit 1: a string
-// longer than max_n; bit 2: more instances than the declared total (the
-// queues would overflow; the job is dropped); bit 4: offsets decreasing or
-// past total_bytes (the string is hashed as empty).  Any set bit means the
-// call's digests are invalid: hth_varlen_status reports it.
-struct QueueTable {
-  u64 qb[NCLS + 1];  // queue c occupies job_map[qb[c], qb[c+1])
-};
-struct PlanParams {
-  const uint8_t* data;
-  const u64* off;
-  u64 n, max_n, total;
-  int job_lvl;
-  u32 lmax;
-  const u64* S;
-  u64 R, F0;  // L' = 1 layout: remainder start, finalize start of row 0 (row stride 64)
-  u64* out;
-  int* err;
-  u32* cls_cnt;
-  u64* queues;
-  u64* meta;
-  unsigned long long* totals;
-  u64* ztab;
-  QueueTable Q;
-};
-template <int OUT>
-__global__ void __launch_bounds__(256) plan_tail_kernel(const __grid_constant__ PlanParams P) {
-  constexpr int K = Var<OUT>::k, M = Geo<Var<OUT>>::m, EW = Geo<Var<OUT>>::ew;
-  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
-  constexpr int NKEY = M + K;  // Toeplitz keys R .. R + m + k - 2, plus slack
-  __shared__ u64 key[NKEY];
-  __shared__ u64 tagseed[K];
-  // this half-warp's first string bounds, loaded before the key staging so
-  // the two latencies overlap
-  const u64 s_first = (u64)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4);
-  const u64 f_o0 = s_first < P.n ? P.off[s_first] : 0;
-  const u64 f_o1 = s_first < P.n ? P.off[s_first + 1] : 0;
-  for (int i = threadIdx.x; i < NKEY; i += blockDim.x) key[i] = __ldg(P.S + P.R + i);
-  if (threadIdx.x < K) tagseed[threadIdx.x] = __ldg(P.S + P.F0 + 64ull * threadIdx.x);
-  // zero-slot table: one thread per (L, l, r) sums its 7 slots and writes the
-  // suffix sums for digits 0..7
-  const u64 nz = (u64)K * P.lmax * P.lmax;
-  for (u64 x = (u64)blockIdx.x * blockDim.x + threadIdx.x; x < nz; x += (u64)gridDim.x * blockDim.x) {
-    const u32 r = (u32)(x % K), l = (u32)(x / K % P.lmax), L = (u32)(x / K / P.lmax) + 1;
-    if (l >= L) continue;
-    const u64 F = (u64)EW + 7ull * L * K + 64ull * L * r + 56ull * l;  // seed_layout (hasher.py:130-153)
-    u64* z = P.ztab + ztab_base(L, K) + (u64)l * 8 * K + r;
-    u64 part[7];  // all 56 seed loads in flight at once
-#pragma unroll
-    for (int slot = 0; slot < 7; slot++) {
-      part[slot] = 0;
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const u64 sw = __ldg(P.S + F + 8 * slot + j);
-        part[slot] += (u64)(u32)sw * (u64)(u32)(sw >> 32);  // NH(0, s)
-      }
-    }
-    u64 acc = 0;
-    z[7 * K] = 0;
-#pragma unroll
-    for (int slot = 6; slot >= 0; slot--) {
-      acc += part[slot];
-      z[slot * K] = acc;
-    }
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, g = lane & 15;
-  const int myidx = scatter_index<K>(g);
-  const u64 per = 1ull << (3 * P.job_lvl);
-  const u64 halves = (u64)gridDim.x * (blockDim.x >> 4);
-  // both halves of a warp iterate together (the reduction shuffles are warp-wide)
-  for (u64 s = (u64)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); s < ((P.n + 1) & ~1ull); s += halves) {
-    const bool live = s < P.n;
-    const bool first = s == s_first;
-    const u64 o0 = live ? (first ? f_o0 : P.off[s]) : 0;
-    const u64 o1 = live ? (first ? f_o1 : P.off[s + 1]) : 0;
-    u64 n = o1 - o0;
-    if (o1 < o0 || o1 > P.total) {
-      if (g == 0) atomicOr(P.err, 4);
-      n = 0;
-    }
-    if (n > P.max_n) {
-      if (g == 0) atomicOr(P.err, 1);
-      n = P.max_n;
-    }
-    const u64 ni = ((n + 7) >> 3) / M;
-    const bool tail = live && ni == 0;
-    if (live && !tail && g == 0) {
-      const u64 J = job_count(ni, P.job_lvl);
-      u64 w, c;
-      scratch_need(ni, K, P.job_lvl, &w, &c);
-      P.meta[2 * s] = w ? atomicAdd(P.totals, (unsigned long long)w) : 0;
-      P.meta[2 * s + 1] = c ? atomicAdd(P.totals + 1, (unsigned long long)c) : 0;
-      for (u64 q = 0; q < J; q++) {
-        const u64 jn = min(per, ni - q * per);
-        const int cl = jn > 64 ? 64 : (int)jn;
-        const u32 pos = atomicAdd(P.cls_cnt + cl, 1u);
-        if (pos < P.Q.qb[cl + 1] - P.Q.qb[cl]) {
-          u64* rec = P.queues + (P.Q.qb[cl] + pos) * JOB_REC;  // the job's record (decode_job)
-          rec[0] = o0;
-          rec[1] = n;
-          rec[2] = s | (q << 32);
-          rec[3] = 0;
-        } else {
-          atomicSub(P.cls_cnt + cl, 1u);
-          atomicOr(P.err, 2);
-        }
-      }
-    }
-    if (!__any_sync(0xffffffffu, tail)) continue;
-    u64 acc[K];
-#pragma unroll
-    for (int r = 0; r < K; r++) acc[r] = 0;
-    const u32 nw = tail ? (u32)((n + 7) >> 3) : 0;
-    for (u32 t = g; t < nw; t += 16) {
-      // absolute address: the buffer base itself may be unaligned
-      const u64 b = reinterpret_cast<u64>(P.data) + o0 + 8ull * t;
-      const u64* p = reinterpret_cast<const u64*>(b & ~7ull);
-      const u32 sh = (u32)(b & 7) * 8;
-      const u64 rem = n - 8ull * t;
-      u64 x = __ldg(p) >> sh;
-      // the next aligned word only if the string reaches into it (no over-read)
-      if (sh && rem > 8 - (b & 7)) x |= __ldg(p + 1) << (64 - sh);
-      if (rem < 8) x &= (1ull << (8 * rem)) - 1;  // zero-pad the partial last word (hasher.py:179-183)
-#pragma unroll
-      for (int r = 0; r < K; r++) acc[r] = nh_acc(acc[r], x, key[t + r]);
-    }
-    if (g == 0 && tail) {
-#pragma unroll
-      for (int r = 0; r < K; r++) acc[r] = nh_acc(acc[r], n, tagseed[r]);  // finalize over the tag
-    }
-    const u64 tot = half_reduce_scatter<K>(acc, g);
-    if (tail && (g & (16 / KP - 1)) == 0 && myidx < K) P.out[s * K + myidx] = tot;
-  }
-}
-
-// ------------------------------------------------------------ launch config
-template <int OUT> struct KCfg;
-// W warps per CTA, NS ring stages per warp (one 8-instance round each),
-// MINB CTAs per SM the register allocation must allow.
-template <> struct KCfg<16> { static constexpr int W = 4, NS = 2, MINB = 4; };
-#ifndef HTH_V2432_MINB
-#define HTH_V2432_MINB 4
-#endif
-template <> struct KCfg<24> { static constexpr int W = 2, NS = 2, MINB = HTH_V2432_MINB; };
-template <> struct KCfg<32> { static constexpr int W = 2, NS = 2, MINB = HTH_V2432_MINB; };
-#ifndef HTH_V40_W
-#define HTH_V40_W 2
-#endif
-#ifndef HTH_V40_NS
-#define HTH_V40_NS 2
-#endif
-#ifndef HTH_V40_MINB
-#define HTH_V40_MINB 5
-#endif
-template <> struct KCfg<40> { static constexpr int W = HTH_V40_W, NS = HTH_V40_NS, MINB = HTH_V40_MINB; };
-
-template <int OUT, bool PS = false>
-constexpr size_t smem_bytes() {
-  constexpr int M = Geo<Var<OUT>>::m;
-  constexpr size_t SB = ROUND_INST * M * 8 + 32;
-  // ring + mbarriers + parked level-1 group and level-3 accumulator +
-  // claimed-job queue (+ per-job EHC seeds in many-seeds mode), per warp
-  return KCfg<OUT>::W * (KCfg<OUT>::NS * (SB + 8) + 9 * Var<OUT>::k * 8 * 8 + (KCfg<OUT>::NS + 4) * 8 * JOB_REC +
-                         (PS ? 2 * MAX_EW * 4 : 0)) +
-         (NCLS + 1) * 4 + NCLS * 8;  // + varlen class table (per CTA)
-}
-
-int sm_count(int dev) {
-  static std::mutex mu;
-  static std::vector<int> cache;
-  std::lock_guard<std::mutex> g(mu);
-  if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
-  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
-  return cache[dev];
-}
-
-// Resident CTAs per SM of `kern` at (tpb, smem) on the current device; the
-// dynamic shared-memory limit is raised once per (kernel, device, smem) and
-// the answer cached, keeping the per-call host path to the launch itself.
-int occupancy(const void* kern, int tpb, size_t smem, int* dev_out, int* occ_out) {
-  static std::mutex mu;
-  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
-  static std::map<std::pair<const void*, int>, size_t> limit;  // the attribute is per kernel: only raise it
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  *dev_out = dev;
-  const auto key = std::make_tuple(kern, dev, smem, tpb);
-  std::lock_guard<std::mutex> g(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) {
-    *occ_out = it->second;
-    return HTH_OK;
-  }
-  size_t& lim = limit[std::make_pair(kern, dev)];
-  if (smem > lim) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    lim = smem;
-  }
-  int o = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, tpb, smem));
-  cache[key] = *occ_out = std::max(o, 1);
-  return HTH_OK;
-}
-
-template <int OUT, bool VARLEN, bool AL8, bool PS = false>
-int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
-  constexpr int W = KCfg<OUT>::W, NS = KCfg<OUT>::NS;
-  auto kern = hash_kernel<OUT, VARLEN, W, NS, KCfg<OUT>::MINB, AL8, PS>;
-  const size_t smem = smem_bytes<OUT, PS>();
-  int dev = 0, occ = 1;
-  if (int rc = occupancy((const void*)kern, W * 32, smem, &dev, &occ)) return rc;
-  u64 grid = (u64)sm_count(dev) * occ;
-  const u64 need = ceil_div(n_jobs_bound, W);
-  if (need < grid) grid = need;
-  if (grid == 0) grid = 1;
-  kern<<<(unsigned)grid, W * 32, smem, st>>>(P);
-  CK(cudaGetLastError());
-  return HTH_OK;
-}
-
-#ifndef HTH_TAIL_NS
-#define HTH_TAIL_NS 1
-#endif
-#ifndef HTH_TAIL_STAGE
-#define HTH_TAIL_STAGE 8192
-#endif
-// NS stages of GP string pairs per warp; measured on config 3 (1 KiB strings):
-// one 8 KiB stage per warp streams best (6.33 TB/s vs 6.21 for 2 x 4 KiB and
-// 5.5 for 4 x 2 KiB), more than 64 KiB per 8-warp CTA costs occupancy
-template <int OUT, int CPT, bool MASKED, int GP>
-int launch_tail_g(const TailParams& P, cudaStream_t st) {
-  constexpr int NS = HTH_TAIL_NS, TPB = 256;
-  auto kern = tail_kernel<OUT, CPT, MASKED, NS, GP>;
-  const u64 sby = (GP * 2 * P.stride + 127) & ~127ull;
-  const size_t smem = (TPB / 32) * NS * (sby + 8);
-  if (smem > 227 * 1024) return fail(HTH_EINVAL, "tail kernel stage too large");
-  int dev = 0, occ = 1;
-  if (int rc = occupancy((const void*)kern, TPB, smem, &dev, &occ)) return rc;
-  const u64 groups = ceil_div((P.n_strings + 1) / 2, (u64)GP);
-  u64 grid = (u64)sm_count(dev) * std::max(occ, 1);
-  const u64 need = ceil_div(groups, TPB / 32);
-  if (need < grid) grid = need;
-  kern<<<(unsigned)std::max<u64>(grid, 1), TPB, smem, st>>>(P);
-  CK(cudaGetLastError());
-  return HTH_OK;
-}
-template <int OUT, int CPT, bool MASKED>
-int launch_tail(const TailParams& P, cudaStream_t st) {
-  const u64 pair = 2 * P.stride;
-  if (4 * pair <= HTH_TAIL_STAGE) return launch_tail_g<OUT, CPT, MASKED, 4>(P, st);
-  if (2 * pair <= HTH_TAIL_STAGE) return launch_tail_g<OUT, CPT, MASKED, 2>(P, st);
-  return launch_tail_g<OUT, CPT, MASKED, 1>(P, st);
-}
-
-// chunks per lane of the instantiation that serves nch 16-byte chunks
-inline int tail_cpt(u64 nch) {
-  const u64 cpt = ceil_div(nch, 16);
-  return cpt <= 1 ? 1 : (cpt <= 2 ? 2 : (cpt <= 4 ? 4 : 6));
-}
-template <int OUT, bool MASKED>
-int dispatch_tail_m(const TailParams& P, u64 nch, cudaStream_t st) {
-  switch (tail_cpt(nch)) {
-    case 1: return launch_tail<OUT, 1, MASKED>(P, st);
-    case 2: return launch_tail<OUT, 2, MASKED>(P, st);
-    case 4: return launch_tail<OUT, 4, MASKED>(P, st);
-  }
-  return launch_tail<OUT, 6, MASKED>(P, st);
-}
-template <int OUT>
-int dispatch_tail(const TailParams& P, u64 nch, cudaStream_t st) {
-  // the unmasked body processes exactly 16 * CPT whole chunks per string:
-  // anything else (a partial last chunk, or fewer chunks than the
-  // instantiation covers, e.g. 80 chunks on the CPT = 6 body) is masked
-  const bool masked = (P.n_bytes % 16) != 0 || nch != 16ull * tail_cpt(nch);
-  return masked ? dispatch_tail_m<OUT, true>(P, nch, st) : dispatch_tail_m<OUT, false>(P, nch, st);
-}
-
-#ifndef HTH_SMALL_STAGE
-#define HTH_SMALL_STAGE 8704
-#endif
-template <int OUT, int G>
-int launch_small(const Params& P, cudaStream_t st) {
-  constexpr int W = KCfg<OUT>::W, NS = 2;
-  auto kern = small_kernel<OUT, G, W, NS, KCfg<OUT>::MINB>;
-  const u64 sby = (G * P.stride + 16 + 127) & ~127ull;
-  const size_t smem = W * NS * (sby + 8);
-  int dev = 0, occ = 1;
-  if (int rc = occupancy((const void*)kern, W * 32, smem, &dev, &occ)) return rc;
-  u64 grid = (u64)sm_count(dev) * std::max(occ, 1);
-  const u64 need = ceil_div(ceil_div(P.n_strings, (u64)G), (u64)W);
-  if (need < grid) grid = need;
-  kern<<<(unsigned)std::max<u64>(grid, 1), W * 32, smem, st>>>(P);
-  CK(cudaGetLastError());
-  return HTH_OK;
-}
-// strings per warp stage: about HTH_SMALL_STAGE bytes per contiguous copy,
-// fewer when the batch would not give every resident warp two stages
-template <int OUT>
-int dispatch_small(const Params& P, cudaStream_t st) {
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  const u64 slots = 2ull * sm_count(dev) * KCfg<OUT>::W * KCfg<OUT>::MINB;
-  int g = 4 * P.stride <= HTH_SMALL_STAGE ? 4 : (2 * P.stride <= HTH_SMALL_STAGE ? 2 : 1);
-  while (g > 1 && ceil_div(P.n_strings, (u64)g) < slots) g >>= 1;
-  if (g == 4) return launch_small<OUT, 4>(P, st);
-  if (g == 2) return launch_small<OUT, 2>(P, st);
-  return launch_small<OUT, 1>(P, st);
-}
 // small_kernel applies: one level (1..7 instances), aligned strings packed
 // closely, and the partial final word (if any) in the tail, not in an instance
 bool small_ok(const VarInfo& v, u64 n_inst, u64 stride, u64 n_bytes, const void* data) {
@@ -471,32 +186,32 @@ bool small_ok(const VarInfo& v, u64 n_inst, u64 stride, u64 n_bytes, const void*
          stride <= n_bytes + 256 && ((n_bytes & 7) == 0 || nw > n_inst * (u64)v.m);
 }
 
-template <bool VARLEN, bool AL8>
-int dispatch_al(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
+// kernel launches live in the per-variant units kv16/24/32/40.cu (launch.cuh)
+template <template <int> class F, class... A>
+int by_width(int out, A&&... a) {
   switch (out) {
-    case 16: return launch_hash<16, VARLEN, AL8>(P, n_jobs_bound, st);
-    case 24: return launch_hash<24, VARLEN, AL8>(P, n_jobs_bound, st);
-    case 32: return launch_hash<32, VARLEN, AL8>(P, n_jobs_bound, st);
-    case 40: return launch_hash<40, VARLEN, AL8>(P, n_jobs_bound, st);
+    case 16: return F<16>::run(a...);
+    case 24: return F<24>::run(a...);
+    case 32: return F<32>::run(a...);
+    case 40: return F<40>::run(a...);
   }
   return fail(HTH_EINVAL, "unsupported output width %d", out);
 }
+template <int OUT> struct HashF { static int run(const Params& P, u64 nj, int kind, cudaStream_t st) { return VarEngine<OUT>::hash(P, nj, kind, st); } };
+template <int OUT> struct TailF { static int run(const TailParams& T, u64 nch, cudaStream_t st) { return VarEngine<OUT>::tail(T, nch, st); } };
+template <int OUT> struct SmallF { static int run(const Params& P, cudaStream_t st) { return VarEngine<OUT>::small(P, st); } };
+template <int OUT> struct PlanF { static int run(const PlanParams& Q, unsigned grid, cudaStream_t st) { return VarEngine<OUT>::plan(Q, grid, st); } };
+template <int OUT> struct MergeF { static int run(const MergeParams& M, cudaStream_t st) { return VarEngine<OUT>::merge(M, st); } };
 // fixed batches whose strings all start 8-byte aligned get the aligned-only kernel
 template <bool VARLEN>
 int dispatch(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
-  if (!VARLEN && (reinterpret_cast<uintptr_t>(P.data) % 8) == 0 && P.stride % 8 == 0)
-    return dispatch_al<false, true>(out, P, n_jobs_bound, st);
-  return dispatch_al<VARLEN, false>(out, P, n_jobs_bound, st);
+  int kind = HK_VARLEN;
+  if (!VARLEN) kind = (reinterpret_cast<uintptr_t>(P.data) % 8) == 0 && P.stride % 8 == 0 ? HK_FIXED_AL8 : HK_FIXED;
+  return by_width<HashF>(out, P, n_jobs_bound, kind, st);
 }
 // per-string seeds (many-seeds seam)
 int dispatch_ps(int out, const Params& P, u64 n_jobs_bound, cudaStream_t st) {
-  switch (out) {
-    case 16: return launch_hash<16, false, false, true>(P, n_jobs_bound, st);
-    case 24: return launch_hash<24, false, false, true>(P, n_jobs_bound, st);
-    case 32: return launch_hash<32, false, false, true>(P, n_jobs_bound, st);
-    case 40: return launch_hash<40, false, false, true>(P, n_jobs_bound, st);
-  }
-  return fail(HTH_EINVAL, "unsupported output width %d", out);
+  return by_width<HashF>(out, P, n_jobs_bound, (int)HK_PS, st);
 }
 
 // A failed launch must not leave a half-used workspace behind: its
@@ -889,20 +604,10 @@ int hth_hash_fixed(int output_bytes, const void* d_data, uint64_t n_strings, uin
       T.tag[r] = (u64)a * b;
     }
     const u64 nch = (n_bytes + 15) / 16;
-    switch (output_bytes) {
-      case 16: return dispatch_tail<16>(T, nch, st);
-      case 24: return dispatch_tail<24>(T, nch, st);
-      case 32: return dispatch_tail<32>(T, nch, st);
-      case 40: return dispatch_tail<40>(T, nch, st);
-    }
+    return by_width<TailF>(output_bytes, T, nch, st);
   }
   if (small_ok(v, f.n_inst, stride_bytes, n_bytes, d_data)) {
-    switch (output_bytes) {
-      case 16: return dispatch_small<16>(P, st);
-      case 24: return dispatch_small<24>(P, st);
-      case 32: return dispatch_small<32>(P, st);
-      case 40: return dispatch_small<40>(P, st);
-    }
+    return by_width<SmallF>(output_bytes, P, st);
   }
   uint8_t* ws = (uint8_t*)d_workspace;
   P.scratch = (u64*)ws;
@@ -1004,13 +709,7 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   Q.ztab = (u64*)(ws + p.off_ztab);
   Q.Q = p.Q;
   const unsigned pb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 16), (u64)sm_count(dev) * 16));
-  switch (output_bytes) {
-    case 16: plan_tail_kernel<16><<<pb, 256, 0, st>>>(Q); break;
-    case 24: plan_tail_kernel<24><<<pb, 256, 0, st>>>(Q); break;
-    case 32: plan_tail_kernel<32><<<pb, 256, 0, st>>>(Q); break;
-    case 40: plan_tail_kernel<40><<<pb, 256, 0, st>>>(Q); break;
-  }
-  CK(cudaGetLastError());
+  if (int rc = by_width<PlanF>(output_bytes, Q, pb, st)) return rc;
   Params P{};
   P.data = (const uint8_t*)d_data;
   P.n_strings = n_strings;
@@ -1200,14 +899,7 @@ int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const
   M.tmp = (u64*)d_workspace;
   M.out = d_out;
   cudaStream_t st = (cudaStream_t)stream;
-  switch (output_bytes) {
-    case 16: merge_kernel<16><<<1, 256, 0, st>>>(M); break;
-    case 24: merge_kernel<24><<<1, 256, 0, st>>>(M); break;
-    case 32: merge_kernel<32><<<1, 256, 0, st>>>(M); break;
-    case 40: merge_kernel<40><<<1, 256, 0, st>>>(M); break;
-  }
-  CK(cudaGetLastError());
-  return HTH_OK;
+  return by_width<MergeF>(output_bytes, M, st);
 }
 
 // Strings longer than kChunk from host memory: each is streamed in slices
