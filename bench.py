@@ -2,7 +2,8 @@
 """HalftimeHash B200 benchmark (driver contract: one JSON line on rank 0).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload cfg4] [--no-extra] [--e2e-steps E]
+                  [--workload cfg1|cfg2|cfg3|cfg4|cfg5] [--no-extra] [--e2e-steps E]
+                  [--exchange auto|flags|p2p|nccl]
 
 Headline workload: config 4 of BASELINE.json -- 8192 strings x 1 MiB per GPU
 (8 GiB, 40-byte variant), the largest batch config and the one quoted per GPU
@@ -10,13 +11,19 @@ and per box; strings are sharded round-robin across ranks (weak scaling, no
 data-path collective).  A "step" is one pass of the hash over the whole
 batch: exactly one hash_kernel launch.  Inputs (8 GiB) exceed L2 (126 MB),
 so no flush is needed between steps.  At N=1 rank 0 also measures the other
-configs (cfg1, cfg2, cfg3, cfg5) into "workloads" (cfg1/cfg2 with an L2
-flush between timed iterations).
+configs (cfg1, cfg2, cfg3, cfg5, and config 5's multi-GPU exchange emulated
+on one GPU) into "workloads" (cfg1/cfg2 with an L2 flush between timed
+iterations).
 
---impl reference times the reference's CPU algorithm (the numpy restatement
-oracle/oracle_np.py of halftimehash's lane engine, hasher.py:331-413; the
-reference itself is Python and cannot travel to the GPU box) on all host
-cores over a bounded sample of the same workload.
+--gpus N > 1 without torchrun's environment re-launches this script under
+``torch.distributed.run --nproc-per-node N`` (127.0.0.1); under torchrun,
+WORLD_SIZE must equal --gpus.  Config 5 on N > 1 GPUs splits the one string
+across the ranks (strong scaling) with the in-stream peer-flag exchange.
+
+--impl reference times the reference's CPU implementation on all host cores
+over a bounded sample of the same workload: the reference package itself
+(halftimehash 0.1.0 ``_hash_words_np``, hasher.py:331-413, installed in
+baseline/_ref) when present, else its numpy restatement oracle/oracle_np.py.
 """
 
 from __future__ import annotations
@@ -41,6 +48,30 @@ import workloads as wl  # noqa: E402
 
 METRIC = "GB/s hashed"
 UNIT = "GB/s"
+
+# the dominant kernel of each workload (launch configuration picked by the C-ABI)
+KERNELS = {
+    "cfg1": "small_kernel<24, G=1, W=2, NS=2, MINB=4> (one launch per step)",
+    "cfg2": "per variant: plan_tail_kernel<w> + hash_kernel<w, varlen> (4 variants on 4 streams, one CUDA graph)",
+    "cfg3": "tail_kernel<32, CPT=4, unmasked, NS=1, GP=4> (one launch per step)",
+    "cfg4": "hash_kernel<40, fixed, W=2, NS=2, MINB=5, AL8> (one launch per step)",
+    "cfg5": "hash_kernel<16, fixed, W=4, NS=2, MINB=4, AL8> (one launch per step)",
+}
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_pkg():
+    """The reference package (halftimehash 0.1.0) if installed in baseline/_ref."""
+    if not os.path.isdir(os.path.join(REF_DIR, "halftimehash")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import halftimehash
+
+        return halftimehash
+    except Exception:
+        return None
 
 
 def _peaks():
@@ -125,17 +156,44 @@ _CPU_SAMPLE = {}
 
 def _cpu_task(arg):
     """Hash worker i's next `count` pre-generated strings (from `start`, cyclic)
-    with the numpy oracle (the pool is inherited via fork)."""
-    from oracle import oracle_np as o
-
+    with the reference's batched engine (or its numpy restatement); the pool
+    is inherited via fork."""
     i, start, count = arg
-    v, n, S, pool = _CPU_SAMPLE["v"], _CPU_SAMPLE["n"], _CPU_SAMPLE["S"], _CPU_SAMPLE["words"][i]
+    n, pool = _CPU_SAMPLE["n"], _CPU_SAMPLE["words"][i]
     if start + count <= pool.shape[0]:
         words = pool[start:start + count]
     else:
         words = pool[(start + np.arange(count)) % pool.shape[0]]
-    o.hash_batch(v, words, n, S)
+    if _CPU_SAMPLE["ref"] is not None:
+        R = _CPU_SAMPLE["ref"]
+        R.hasher._hash_words_np(words, n, _CPU_SAMPLE["ref_seed"].words_np, _CPU_SAMPLE["ref_params"])
+    else:
+        from oracle import oracle_np as o
+
+        o.hash_batch(_CPU_SAMPLE["v"], words, n, _CPU_SAMPLE["S"])
     return count * n
+
+
+def _cpu_task_varlen(arg):
+    """Config 2 on the CPU: the reference hashes each string with hash_bytes
+    (lengths differ), all four variants; worker i takes strings
+    i, i + cores, ... of its share of the batch."""
+    i, cores = arg
+    data, off, R = _CPU_SAMPLE["data"], _CPU_SAMPLE["off"], _CPU_SAMPLE["ref"]
+    total = 0
+    for w in (16, 24, 32, 40):
+        if R is not None:
+            p, seed = _CPU_SAMPLE["ref_params"][w], _CPU_SAMPLE["ref_seed"][w]
+        for s in range(i, len(off) - 1, cores):
+            b = data[int(off[s]):int(off[s + 1])]
+            if R is not None:
+                R.hash_bytes(b, seed, p)
+            else:
+                from oracle import oracle_np as o
+
+                o.hash_bytes(_CPU_SAMPLE["v"][w], b, _CPU_SAMPLE["S"][w])
+            total += len(b)
+    return total
 
 
 # strings per core per pass of the CPU arm (~4 MiB: the numpy port's best granularity)
@@ -147,46 +205,82 @@ CPU_POOL_BYTES = 64 << 20
 
 
 class CpuBaseline:
-    """The reference's CPU algorithm (numpy restatement of hasher.py:331-413)
-    on `cores` forked processes.  Each process holds a pool of >= 64 MiB of
-    distinct strings of the workload, generated before any timing; rate()
-    times one pass in which every process hashes its next `per_core` strings
-    (cyclic), so small samples are not served from cache."""
+    """The reference's CPU path on `cores` forked processes: the reference
+    package's own ``_hash_words_np`` (hasher.py:331-413) when it is installed
+    in baseline/_ref (kind "reference"), else its numpy restatement
+    oracle/oracle_np.py (kind "port", bit-identical, ~1.3x faster).  Each
+    process holds a pool of >= 64 MiB of distinct strings of the workload,
+    generated before any timing; rate() times one pass in which every process
+    hashes its next `per_core` strings (cyclic), so small samples are not
+    served from cache.  Config 2: per-string hash_bytes over the batch, all
+    four variants, strings dealt round-robin to the processes."""
 
-    def __init__(self, workload: str, per_core: int, cores: int):
+    def __init__(self, workload: str, per_core: int, cores: int, use_reference: bool = True):
         from oracle import oracle_np as o
 
-        cfg = wl.CONFIGS[workload]
-        w, n = cfg["variant"], cfg["n_bytes"]
-        if workload == "cfg5":  # one huge string: time 16 MiB pieces of it
-            n = 16 << 20
-        v = o.variant(w)
-        assert n % 8 == 0
-        per_pool = max(per_core, -(-CPU_POOL_BYTES // n))
-        _CPU_SAMPLE.update(v=v, n=n, S=o.splitmix_words(o.master_fold(wl.MASTER), 0, o.seed_words_needed(v, n)))
-        _CPU_SAMPLE["words"] = [
-            o.words_from_bytes(wl.host_bytes(i * per_pool * n, per_pool * n)).reshape(per_pool, -1)
-            for i in range(cores)]
-        self.cores, self.per_core, self.n, self.w, self.per_pool = cores, per_core, n, w, per_pool
+        R = _reference_pkg() if use_reference else None
+        self.kind = "reference" if R is not None else "port"
+        _CPU_SAMPLE.clear()
+        _CPU_SAMPLE["ref"] = R
+        self.workload = workload
+        self.cores = cores
         self.next = 0
+        if workload == "cfg2":
+            lengths = wl.cfg2_lengths()
+            off = wl.offsets_of(lengths)
+            _CPU_SAMPLE.update(data=wl.host_bytes(0, int(off[-1])), off=off)
+            mx = int(lengths.max())
+            if R is not None:
+                _CPU_SAMPLE["ref_params"] = {w: R.variant(w) for w in (16, 24, 32, 40)}
+                _CPU_SAMPLE["ref_seed"] = {w: R.seed_for_input(wl.MASTER, R.variant(w), mx) for w in (16, 24, 32, 40)}
+            else:
+                _CPU_SAMPLE["v"] = {w: o.variant(w) for w in (16, 24, 32, 40)}
+                _CPU_SAMPLE["S"] = {w: o.splitmix_words(o.master_fold(wl.MASTER), 0,
+                                                        o.seed_words_needed(o.variant(w), mx)) for w in (16, 24, 32, 40)}
+            self.n, self.w, self.per_core, self.per_pool = int(off[-1]), "16/24/32/40", 0, 0
+        else:
+            cfg = wl.CONFIGS[workload]
+            w, n = cfg["variant"], cfg["n_bytes"]
+            if workload == "cfg5":  # one huge string: time 16 MiB pieces of it
+                n = 16 << 20
+            v = o.variant(w)
+            assert n % 8 == 0
+            per_pool = max(per_core, -(-CPU_POOL_BYTES // n))
+            _CPU_SAMPLE.update(v=v, n=n, S=o.splitmix_words(o.master_fold(wl.MASTER), 0, o.seed_words_needed(v, n)))
+            if R is not None:
+                _CPU_SAMPLE["ref_params"] = R.variant(w)
+                _CPU_SAMPLE["ref_seed"] = R.seed_for_input(wl.MASTER, R.variant(w), n)
+            _CPU_SAMPLE["words"] = [
+                o.words_from_bytes(wl.host_bytes(i * per_pool * n, per_pool * n)).reshape(per_pool, -1)
+                for i in range(cores)]
+            self.per_core, self.n, self.w, self.per_pool = per_core, n, w, per_pool
         self.pool = mp.get_context("fork").Pool(cores) if cores > 1 else None
 
     def rate(self):
-        args = [(i, self.next, self.per_core) for i in range(self.cores)]
-        self.next = (self.next + self.per_core) % self.per_pool
+        if self.workload == "cfg2":
+            fn, args = _cpu_task_varlen, [(i, self.cores) for i in range(self.cores)]
+        else:
+            fn, args = _cpu_task, [(i, self.next, self.per_core) for i in range(self.cores)]
+            self.next = (self.next + self.per_core) % self.per_pool
         t0 = time.perf_counter()
         if self.pool is None:
-            total = _cpu_task(args[0])
+            total = sum(fn(a) for a in args)
         else:
-            total = sum(self.pool.map(_cpu_task, args, chunksize=1))
+            total = sum(self.pool.map(fn, args, chunksize=1))
         dt = time.perf_counter() - t0
         return total / dt / 1e9, total, dt
 
     def sample(self):
+        engine = ("the reference package itself (halftimehash 0.1.0 from baseline/_ref: _hash_words_np, "
+                  "hasher.py:331-413)" if self.kind == "reference" else
+                  "numpy restatement of hasher.py:331-413 (oracle/oracle_np.py, bit-identical to the reference, "
+                  "~1.3x its single-core speed)")
+        if self.workload == "cfg2":
+            return (f"{self.cores} processes, the whole config-2 batch ({self.n} B, 16384 strings) per pass and "
+                    f"variant, one hash_bytes per string (all 4 variants); {engine.replace('_hash_words_np', 'hash_bytes')}")
         return (f"{self.cores} processes x {self.per_core} strings of {self.n} B (v{self.w}) per pass, "
                 f"each from its own pool of {self.per_pool} distinct pre-generated strings (cyclic, larger "
-                "than the caches); numpy restatement of hasher.py:331-413 (oracle/oracle_np.py, "
-                "bit-identical to the reference, ~1.3x its single-core speed)")
+                f"than the caches); {engine}")
 
     def close(self):
         if self.pool is not None:
@@ -214,12 +308,8 @@ def setup_fixed(hh, torch, workload, rank=0, world=1):
     B = cfg["n_strings"]
     p = hh.variant(w)
     buf = torch.empty(B * n + 64, dtype=torch.uint8, device="cuda")
-    if world == 1:
-        hh.fill_bytes(B * n, wl.DATA_SEED, 0, out=buf)
-    else:  # round-robin: local string i is global string rank + i * world
-        for i in range(B):
-            g = rank + i * world
-            hh.fill_bytes(n, wl.DATA_SEED, g * n // 8, out=buf[i * n:(i + 1) * n + 16])
+    # round-robin: local string i is global string rank + i * world (one launch)
+    hh.fill_strings(B, n, rank, world, wl.DATA_SEED, out=buf)
     seed = hh.seed_for_input(wl.MASTER, p, n)
     st = seed.device_words()
     out = torch.empty((B, p.output_words), dtype=torch.int64, device="cuda")
@@ -304,8 +394,9 @@ def measure_latency(hh, sizes=(64, 4096, 1 << 20, 64 << 20), variant=24, reps=20
     return out
 
 
-def measure_workload(hh, torch, workload, steps, warmup, peak):
-    """N=1 secondary measurement of one config (rank 0 only)."""
+def measure_workload(hh, torch, workload, steps, warmup, peak, barrier=None):
+    """Measurement of one config on this GPU (the secondary configs at N=1;
+    config 2's main line)."""
     res = {"desc": wl.CONFIGS[workload]["desc"]}
     if workload == "cfg2":
         # four variants over the same packed batch: independent pipelines (plan ->
@@ -337,13 +428,15 @@ def measure_workload(hh, torch, workload, steps, warmup, peak):
                 with torch.cuda.stream(side[w]):
                     side[w].wait_event(ev)
                     hh.hash_varlen(buf, d_off, seeds[w], hh.variant(w), max_n_bytes=mx, out=outs[w],
-                                   workspace=wss[w])
+                                   workspace=wss[w], check=False)
             for w in widths:
                 cur.wait_stream(side[w])
 
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
+        for w in widths:  # the device found no bound or offset violation
+            hb.varlen_status(wss[w])
         # correctness of the concurrent path: compare with the serial result
         ref = {w: hh.hash_varlen(buf, d_off, seeds[w], hh.variant(w), max_n_bytes=mx).clone() for w in widths}
         g = torch.cuda.CUDAGraph()
@@ -357,6 +450,8 @@ def measure_workload(hh, torch, workload, steps, warmup, peak):
         flush = make_flush(torch)
         per = []
         stream = torch.cuda.current_stream()
+        if barrier:
+            barrier()
         for _ in range(steps):
             flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -441,7 +536,7 @@ def arm_reference(args, rank, world):
     cores = os.cpu_count() or 1
     per_core = CPU_PER_CORE.get(workload, 4)
     cpu = CpuBaseline(workload, per_core, cores)
-    for _ in range(args.warmup):
+    for _ in range(1 if workload == "cfg2" else args.warmup):
         cpu.rate()
     rates, dts, tot = [], [], 0
     for _ in range(args.steps):
@@ -459,23 +554,44 @@ def arm_reference(args, rank, world):
         "data": "synthetic (splitmix stream, seed 0)",
         "config": {"workload": workload, "desc": cfg["desc"], "variant": cfg["variant"],
                    "bytes_per_step": tot},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": cpu.sample()},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": cpu.kind, "sample": cpu.sample()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+def _rank_report(dist, info):
+    """Every rank's own record (device, busy time, clocks), gathered to all."""
+    if dist is None:
+        return [info]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, info)
+    return out
+
+
+def _comm(dist):
+    if dist is None:
+        return {"backend": None, "world_size": 1}
+    return {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+            "note": "communicator of the barrier / max-over-ranks timing; the hash itself has no data-path collective"}
+
+
 def arm_split(args, rank, world, local_rank, hh, torch, dist):
     """Config 5 on N > 1 GPUs: ONE 16 GiB string split at multiples of 8^c
     instances (hth_slice_plan); each rank generates and hashes its slice in
-    place (hth_hash_slice), the level-c subtree roots and partial digests go
-    to rank 0 -- stored by the slice kernels straight into rank 0's memory
-    through CUDA-IPC peer pointers (--exchange p2p, default; one barrier) or
-    moved by all_gather (--exchange nccl) -- and rank 0 finishes the tree
-    (hth_hash_merge).
-    A step = the whole string: slice kernel + exchange + merge; total work is
-    fixed as N grows (strong scaling)."""
+    place (hth_hash_slice_ex).  Exchange (--exchange):
+      flags (default with one GPU per rank): in-stream -- the slice kernels
+        store their subtree roots and partial digest into rank 0's memory
+        over NVLink (CUDA-IPC peer pointers) and raise a per-rank arrival
+        flag; rank 0's merge kernel waits on the flags in-stream; slots are
+        double-buffered and handed back through a consumed flag.  No host
+        synchronisation, barrier or collective inside the step.
+      p2p: the same peer stores, then a host synchronize + barrier per string
+        (the only safe form when ranks share a GPU).
+      nccl: all_gather of roots/partials.
+    A step = the whole string; total work is fixed as N grows (strong
+    scaling)."""
     from paper_2104_08865_b200 import multi_gpu
 
     peak, peak_src = _peaks()
@@ -488,22 +604,35 @@ def arm_split(args, rank, world, local_rank, hh, torch, dist):
     hh.fill_bytes(b1 - b0, wl.DATA_SEED, b0 // 8, out=buf)
     seed = hh.seed_for_input(wl.MASTER, p, n)
     seed.device_words()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    exchange = args.exchange
+    ids = multi_gpu._device_ids(dev, None)
+    distinct = len(set(ids)) == len(ids)
+    if exchange == "auto":
+        exchange = "flags" if distinct else "p2p"
+    if exchange == "flags" and not distinct:
+        raise SystemExit("--exchange flags needs one GPU per rank (kernels on one device must not wait on each other)")
+    fx = multi_gpu.FlagExchange(plan, seed, dev) if exchange == "flags" else None
     stream = torch.cuda.current_stream()
     kern = []
+    last = {}
 
     def step():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        if args.exchange == "p2p":
-            d = multi_gpu.hash_string_p2p(buf, plan, seed)
+        if fx is not None:
+            last["d"] = fx.step(buf)
+        elif exchange == "p2p":
+            last["d"] = multi_gpu.hash_string_p2p(buf, plan, seed)
         else:
-            d = multi_gpu.hash_string_distributed(buf, plan, seed)
+            last["d"] = multi_gpu.hash_string_distributed(buf, plan, seed)
         b.record(stream)
         kern.append((a, b))
-        return d
 
     for _ in range(args.warmup):
-        digest = step()
+        step()
+    if fx is not None:
+        fx.check()
     torch.cuda.synchronize()
     sampler = ClockSampler(local_rank)
     sampler.start()
@@ -515,17 +644,27 @@ def arm_split(args, rank, world, local_rank, hh, torch, dist):
     wall0 = time.time()
     t0.record(stream)
     for _ in range(args.steps):
-        digest = step()
+        step()
     t1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     wall1 = time.time()
     time.sleep(0.2)
     sampler.stop()
-    t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
+    if fx is not None:
+        fx.check()
+    mine_ms = t0.elapsed_time(t1)
+    t = torch.tensor([mine_ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item()) / args.steps
     step_ms = statistics.mean(a.elapsed_time(b) for a, b in kern)
+    ranks = _rank_report(dist, {"rank": rank, "device": ids[rank], "slice_bytes": b1 - b0,
+                                "busy_ms_per_step": mine_ms / args.steps, "step_event_ms": step_ms,
+                                "clocks": sampler.summary(wall0, wall1)})
+    digest = None
+    if rank == 0:
+        d = last["d"]
+        digest = d.cpu().numpy().view(np.uint64).copy() if hasattr(d, "cpu") else d
     check = None
     if rank == 0 and not args.no_check:
         from oracle import c as coracle
@@ -534,6 +673,12 @@ def arm_split(args, rank, world, local_rank, hh, torch, dist):
         want = coracle.hash_huge(w, host, seed.words_np(0, seed.capacity))
         check = bool(np.array_equal(digest, want))
     if rank == 0:
+        ex_desc = {
+            "flags": "in-stream: slice kernels store roots/partials into rank 0's memory (CUDA IPC over NVLink) and "
+                     "raise per-rank arrival flags; rank 0's merge kernel waits on them; no host sync in the step",
+            "p2p": "slice kernels store roots/partials into rank 0's memory (CUDA IPC) + host sync + barrier",
+            "nccl": "all_gather of roots/partials",
+        }[exchange]
         line = {
             "metric": METRIC, "value": n / (ms / 1e3) / 1e9, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -542,23 +687,101 @@ def arm_split(args, rank, world, local_rank, hh, torch, dist):
                        "sharding": f"one string split at multiples of 8^{plan.level} instances",
                        "slices_instances": list(plan.bounds), "frontier_roots": plan.n_frontier,
                        "l2": "inputs larger than L2 (126 MB); no flush needed",
-                       "exchange": ("slice kernels store roots/partials into rank 0's memory (CUDA IPC, NVLink) + barrier"
-                                    if args.exchange == "p2p" else "all_gather of roots/partials"),
-                       "parallelism": f"dp{world} slices + root exchange + merge on rank 0"},
+                       "exchange": ex_desc, "parallelism": f"dp{world} slices + root exchange + merge on rank 0"},
             "roofline": {"bound": "hbm", "achieved": (b1 - b0) / (step_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": (b1 - b0) / (step_ms / 1e3) / 1e9 / peak, "traffic": None,
-                         "kernel": "rank 0 step: hash_kernel<16> slice + all_gather + merge_kernel",
+                         "kernel": "rank 0 step: hash_kernel<16> slice + exchange + merge_kernel",
                          "kernel_ms": step_ms, "peak_source": peak_src},
             "cpu_baseline": None,
             "e2e": None,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": (2 if exchange != "nccl" else 2) * args.steps,
             "clocks": sampler.summary(wall0, wall1),
+            "ranks": ranks,
+            "comm": _comm(dist),
             "oracle_check": check,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
     return 0
+
+
+def measure_exchange_emulated(hh, torch, n_slices=8, steps=5):
+    """Config 5's multi-GPU exchange, emulated on ONE GPU: the n_slices
+    slices of the 16 GiB string run one after another on one stream (the
+    FlagExchange protocol with every rank in this process: slice kernels that
+    raise arrival flags, the merge kernel that waits on them -- already
+    raised, since nothing runs concurrently -- and the consumed-flag slot
+    hand-back), each launch timed with CUDA events.  On N GPUs the slices run
+    concurrently, so a step costs max(slice) + merge; the merge (and the
+    flag handling inside it) is the exchange's whole on-device cost."""
+    from paper_2104_08865_b200 import multi_gpu
+
+    cfg = wl.CONFIGS["cfg5"]
+    w, n = cfg["variant"], cfg["n_bytes"]
+    p = hh.variant(w)
+    plan = multi_gpu.slice_plan(p, n, n_slices)
+    buf = torch.empty(n + 64, dtype=torch.uint8, device="cuda")
+    hh.fill_bytes(n, wl.DATA_SEED, 0, out=buf)
+    seed = hh.seed_for_input(wl.MASTER, p, n)
+    seed.device_words()
+    stream = torch.cuda.current_stream()
+    state, marks, epoch = None, [], 0
+
+    def mark(tag):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        marks.append((tag, e))
+
+    for it in range(steps + 2):
+        epoch += 1
+        if it == 2:
+            marks.clear()
+        d, state = multi_gpu.hash_string_emulated(buf, plan, seed, epoch, state, mark=mark)
+    torch.cuda.synchronize()
+    slices, merges = [], []
+    for (ta, a), (tb, b) in zip(marks, marks[1:]):
+        if ta.startswith("slice"):
+            slices.append(a.elapsed_time(b))
+        elif ta == "merge" and tb == "end":
+            merges.append(a.elapsed_time(b))
+    digest = d.cpu().numpy().view(np.uint64).copy()
+    status = int(state["status"].item())
+    from oracle import c as coracle
+
+    host = coracle.splitmix(wl.DATA_SEED, 0, n // 8).view(np.uint8)
+    want = coracle.hash_huge(w, host, seed.words_np(0, seed.capacity))
+    per_step = np.array(slices).reshape(steps, n_slices)
+    slice_max = float(per_step.max(axis=1).mean())
+    merge = float(statistics.mean(merges))
+    del buf
+    torch.cuda.empty_cache()
+    return {"desc": f"config 5 split into {n_slices} slices (the {n_slices}-GPU plan) on one GPU, sequentially",
+            "frontier_level": plan.level, "frontier_roots": plan.n_frontier,
+            "slice_ms_mean": float(per_step.mean()), "slice_ms_max": slice_max,
+            "merge_ms": merge, "projected_step_ms": slice_max + merge,
+            "exchange_frac_of_step": merge / (slice_max + merge),
+            "projected_gbs": n / ((slice_max + merge) / 1e3) / 1e9,
+            "digest_matches_oracle": bool(np.array_equal(digest, want)), "wait_status": status,
+            "note": "exchange = merge kernel incl. its flag waits and slot hand-back; the slices' flag stores are "
+                    "inside the slice kernels' times"}
+
+
+def measure_sustained(hh, torch, workload, steps, local_rank):
+    """The headline kernel over a long run (board power cap reached)."""
+    ctx = setup_fixed(hh, torch, workload)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.2)
+    total_ms, per, (w0, w1) = run_fixed(hh, torch, ctx, steps, 5)
+    time.sleep(0.1)
+    sampler.stop()
+    ms = total_ms / steps
+    res = {"steps": steps, "value": ctx["B"] * ctx["n"] / (ms / 1e3) / 1e9, "ms_per_step": ms,
+           "clocks": sampler.summary(w0, w1)}
+    del ctx
+    torch.cuda.empty_cache()
+    return res
 
 
 def arm_ours(args, rank, world, local_rank):
@@ -583,45 +806,65 @@ def arm_ours(args, rank, world, local_rank):
         return arm_split(args, rank, world, local_rank, hh, torch, dist)
     peak, peak_src = _peaks()
     workload = args.workload
-    ctx = setup_fixed(hh, torch, workload, rank, world)
-    k = ctx["p"].output_words
+    dev_name = torch.cuda.get_device_name(local_rank)
     sampler = ClockSampler(local_rank)
-    sampler.start()
-    time.sleep(0.3)
-    # warm-up, then barrier + synchronize on both sides of exactly K timed steps
-    small = ctx["B"] * ctx["n"] < (256 << 20)  # L2-sized input (config 1): flush L2 before every step
-    total_ms, per, (w0, w1) = run_fixed(hh, torch, ctx, args.steps, args.warmup,
-                                        flush=make_flush(torch) if small else None,
-                                        barrier=dist.barrier if dist else None)
-    time.sleep(0.2)
-    sampler.stop()
+    check = None
+    if workload == "cfg2":
+        # every rank hashes its own replica of the varlen batch (strings of
+        # config 2 are not sharded by BASELINE; N > 1 = N independent replicas)
+        sampler.start()
+        time.sleep(0.3)
+        w0 = time.time()
+        r2 = measure_workload(hh, torch, "cfg2", args.steps, args.warmup, peak, barrier=dist.barrier if dist else None)
+        w1 = time.time()
+        time.sleep(0.2)
+        sampler.stop()
+        B, n, k = 16384, r2["bytes_per_step"], 0
+        total_ms = r2["ms_per_step"] * args.steps
+        kernel_ms = r2["ms_per_step"]
+        algo = r2["bytes_per_step"] + 4 * 16384 * 28 * 8 // 7  # input bytes of 4 variants + their digests
+        check = r2.get("graph_matches_serial")
+        value_bytes = r2["bytes_per_step"]
+    else:
+        ctx = setup_fixed(hh, torch, workload, rank, world)
+        k = ctx["p"].output_words
+        sampler.start()
+        time.sleep(0.3)
+        # warm-up, then barrier + synchronize on both sides of exactly K timed steps
+        small = ctx["B"] * ctx["n"] < (256 << 20)  # L2-sized input (config 1): flush L2 before every step
+        total_ms, per, (w0, w1) = run_fixed(hh, torch, ctx, args.steps, args.warmup,
+                                            flush=make_flush(torch) if small else None,
+                                            barrier=dist.barrier if dist else None)
+        time.sleep(0.2)
+        sampler.stop()
+        kernel_ms = statistics.mean(per)  # one kernel launch per step, events on its stream
+        B, n = ctx["B"], ctx["n"]
+        value_bytes = B * n
+        algo = _algo_bytes(workload, B, n, k)
+        # digests stay sharded; rank 0 checks a sample of its digests against the oracle
+        if rank == 0 and not args.no_check:
+            from oracle import c as coracle
+
+            nchk = min(4, B)
+            got = ctx["out"][:nchk].cpu().numpy().view(np.uint64)
+            host = _stream_strings([rank + i * world for i in range(nchk)], n)
+            S = ctx["seed"].words_np(0, ctx["seed"].capacity)
+            want = coracle.hash_fixed(ctx["w"], host, nchk, n, n, S)
+            check = bool(np.array_equal(got, want))
+        del ctx
+        torch.cuda.empty_cache()
     clocks = sampler.summary(w0, w1)
-    kernel_ms = statistics.mean(per)  # one hash_kernel launch per step, events on its stream
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    ms = total_ms / args.steps
-    B, n = ctx["B"], ctx["n"]
-    value = world * B * n / (ms / 1e3) / 1e9
-    algo = _algo_bytes(workload, B, n, k)
+    ms = float(t.item()) / args.steps
+    value = world * value_bytes / (ms / 1e3) / 1e9
     achieved = algo / (kernel_ms / 1e3) / 1e9
-    # digests stay sharded; rank 0 checks a sample of its digests against the oracle
-    check = None
-    if rank == 0 and not args.no_check:
-        from oracle import c as coracle
-        from oracle import oracle_np as o
-
-        nchk = min(4, B)
-        got = ctx["out"][:nchk].cpu().numpy().view(np.uint64)
-        host = _stream_strings([rank + i * world for i in range(nchk)], n)
-        S = ctx["seed"].words_np(0, ctx["seed"].capacity)
-        want = coracle.hash_fixed(ctx["w"], host, nchk, n, n, S)
-        check = bool(np.array_equal(got, want))
-    del ctx
-    torch.cuda.empty_cache()
+    ranks = _rank_report(dist, {"rank": rank, "device": dev_name, "local_rank": local_rank,
+                                "busy_ms_per_step": total_ms / args.steps, "kernel_ms": kernel_ms,
+                                "clocks": clocks})
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and workload != "cfg2":
         try:
             e2e, e2e_out = e2e_fixed(hh, torch, workload, args.e2e_steps, args.e2e_strings, rank, world, local_rank,
                                      dist)
@@ -644,50 +887,65 @@ def arm_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1:
         if not args.no_extra:
-            for wk in ("cfg1", "cfg2", "cfg3", "cfg5"):
+            for wk in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
+                if wk == workload:
+                    continue
                 try:
                     extra[wk] = measure_workload(hh, torch, wk, steps=max(5, min(args.steps, 50)), warmup=3,
                                                  peak=peak)
                 except Exception as ex:  # pragma: no cover
                     extra[wk] = {"error": repr(ex)}
-            try:
-                extra["latency"] = measure_latency(hh)
-            except Exception as ex:  # pragma: no cover
-                extra["latency"] = {"error": repr(ex)}
+            for name, fn in (("cfg5_exchange_8gpu_emulated", lambda: measure_exchange_emulated(hh, torch)),
+                             ("latency", lambda: measure_latency(hh))):
+                try:
+                    extra[name] = fn()
+                except Exception as ex:  # pragma: no cover
+                    extra[name] = {"error": repr(ex)}
+            if workload != "cfg2":
+                try:
+                    extra["sustained"] = measure_sustained(hh, torch, workload, args.sustained_steps, local_rank)
+                except Exception as ex:  # pragma: no cover
+                    extra["sustained"] = {"error": repr(ex)}
         cores = os.cpu_count() or 1
-        # the reference arm's granularity (the numpy port is fastest on small
-        # batches), median of several passes over fresh strings
+        # the reference arm's granularity (small batches per pass), median of
+        # several passes over fresh strings
         cb = CpuBaseline(workload, CPU_PER_CORE.get(workload, 4), cores)
         cb.rate()
-        runs = [cb.rate() for _ in range(8)]
+        runs = [cb.rate() for _ in range(3 if workload == "cfg2" else 8)]
         cb.close()
         r = statistics.median(x[0] for x in runs)
         # the same algorithm in one process (single process and all cores)
-        c1 = CpuBaseline(workload, CPU_PER_CORE.get(workload, 4), 1)
-        c1.rate()
-        r1 = statistics.median(c1.rate()[0] for _ in range(3))
-        c1.close()
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": cb.sample() + f"; median of 8 passes, {sum(x[2] for x in runs):.2f} s",
+        r1 = None
+        if workload != "cfg2":
+            c1 = CpuBaseline(workload, CPU_PER_CORE.get(workload, 4), 1)
+            c1.rate()
+            r1 = statistics.median(c1.rate()[0] for _ in range(3))
+            c1.close()
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": cb.kind,
+               "sample": cb.sample() + f"; median of {len(runs)} passes, {sum(x[2] for x in runs):.2f} s",
                "single_core_value": r1}
     if rank == 0:
+        cfg = wl.CONFIGS[workload]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (splitmix stream seed 0; seed array seed 1)",
-            "config": {"workload": workload, "desc": wl.CONFIGS[workload]["desc"], "n_strings_per_gpu": B,
-                       "n_bytes": n, "variant": ctx_variant(workload), "sharding": "round-robin by string",
-                       "l2": ("flushed (256 MB write) before every timed step" if small else
-                              "inputs larger than L2 (126 MB); no flush needed"),
+            "config": {"workload": workload, "desc": cfg["desc"], "n_strings_per_gpu": B,
+                       "n_bytes": n if workload != "cfg2" else "varlen", "variant": cfg["variant"],
+                       "sharding": ("replica per GPU" if workload == "cfg2" else "round-robin by string"),
+                       "l2": ("flushed (256 MB write) before every timed step"
+                              if workload in ("cfg1", "cfg2") else "inputs larger than L2 (126 MB); no flush needed"),
                        "parallelism": f"dp{world} (independent strings, no collective)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(workload),
-                         "kernel": "hash_kernel<40, fixed, W=2, NS=2, MINB=5, AL8> (one launch per step)", "kernel_ms": kernel_ms,
+                         "kernel": KERNELS[workload], "kernel_ms": kernel_ms,
                          "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (8 if workload == "cfg2" else 1),
             "clocks": clocks,
+            "ranks": ranks,
+            "comm": _comm(dist),
             "oracle_check": check,
             "workloads": extra,
         }
@@ -702,24 +960,50 @@ def ctx_variant(workload):
     return wl.CONFIGS[workload]["variant"]
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: run this script as N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-strings", type=int, default=0, help="cap e2e batch (0 = full config)")
-    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
-                    help="cfg5 on N > 1 GPUs: how the subtree roots reach rank 0")
+    ap.add_argument("--sustained-steps", type=int, default=300, help="long run of the headline kernel (N=1)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "flags", "p2p", "nccl"],
+                    help="cfg5 on N > 1 GPUs: how the subtree roots reach rank 0 (auto: flags if one GPU per rank)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        return self_launch(args)
+    world = int(env_world or 1)
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; launch {args.gpus} ranks "
+              f"(or run without torchrun and let bench.py launch them)", file=sys.stderr, flush=True)
+        return 2
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         return arm_reference(args, rank, world)

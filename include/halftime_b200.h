@@ -92,6 +92,12 @@ int hth_expand_seed(uint64_t fold, uint64_t start, uint64_t count, uint64_t* d_w
 /* cli.fill_bytes (cli.py:48-53) on the device: n_bytes of the splitmix stream
  * keyed by fill_seed, starting at stream word `word_offset`. */
 int hth_fill_splitmix(uint64_t fill_seed, uint64_t word_offset, uint64_t n_bytes, void* d_dst, void* stream);
+/* One launch for a shard of a packed batch of n_bytes-strings (n_bytes % 8
+ * == 0): local string i (at d_dst + i * dst_stride) = global string
+ * first_string + i * string_step, i.e. stream words from
+ * (first_string + i * string_step) * n_bytes / 8 on. */
+int hth_fill_splitmix_strings(uint64_t fill_seed, uint64_t n_strings, uint64_t n_bytes, uint64_t first_string,
+                              uint64_t string_step, void* d_dst, uint64_t dst_stride, void* stream);
 
 /* ---- batched hash of equal-length strings: the _hash_words_np seam
  *      (hasher.py:331-413) for B = n_strings rows sharing n_bytes.
@@ -167,6 +173,35 @@ int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const
  * passes pointers into it as hth_hash_slice's d_frontier / d_partial, so the
  * slice kernel itself stores its subtree roots and partial digest into rank
  * 0's memory.  hth_ipc_close_handle unmaps (the mapped base). */
+/* In-stream exchange (no host synchronisation on the data path).
+ * hth_hash_slice_ex = hth_hash_slice plus: when the slice is done, its
+ * kernel's last warp stores done_value to *d_done_flag with a system-scope
+ * release after every frontier/partial store of the slice is visible
+ * system-wide (d_done_flag, like d_frontier/d_partial, may be a peer GPU's
+ * memory).  options HTH_SLICE_ACCUMULATE: d_partial already holds zeros
+ * (the merge re-zeroes it), so it is not cleared first.
+ * hth_hash_merge_ex = hth_hash_merge whose kernel first waits until each of
+ * the n_partials flags d_flags[i] >= epoch (system-scope acquire), and after
+ * writing the digest zeroes d_partials and stores epoch to *d_consumed
+ * (release) so producers may reuse the buffers.  A wait longer than
+ * timeout_ns sets *d_status = 1 instead of hanging (digest then invalid).
+ * hth_signal / hth_wait_flag: the same release store / bounded acquire spin
+ * as a one-thread launch.  Waiting kernels must only ever wait on work
+ * running on ANOTHER GPU (or already completed): two ranks sharing one
+ * device are not guaranteed to run concurrently. */
+#define HTH_SLICE_ACCUMULATE 1
+int hth_hash_slice_ex(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
+                      int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
+                      uint64_t* d_frontier, uint64_t* d_partial, uint64_t* d_done_flag, uint64_t done_value,
+                      int options, void* d_workspace, uint64_t workspace_bytes, void* stream);
+int hth_hash_merge_ex(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
+                      uint64_t n_frontier, uint64_t* d_partials, uint64_t n_partials, const uint64_t* d_seed,
+                      uint64_t seed_capacity, uint64_t* d_out, const uint64_t* d_flags, uint64_t epoch,
+                      uint64_t* d_consumed, uint64_t timeout_ns, int* d_status, void* d_workspace,
+                      uint64_t workspace_bytes, void* stream);
+int hth_signal(uint64_t* d_flag, uint64_t value, void* stream);
+int hth_wait_flag(const uint64_t* d_flag, uint64_t value, uint64_t timeout_ns, int* d_status, void* stream);
+
 int hth_ipc_get_handle(const void* d_ptr, uint8_t handle_out[64], uint64_t* offset_out);
 int hth_ipc_open_handle(const uint8_t handle[64], void** d_ptr_out);
 int hth_ipc_close_handle(void* d_ptr);

@@ -39,7 +39,7 @@ __all__ = [
     "Digest", "ErasureCode", "HashParams", "SeedBuffer", "SeedLayout", "SeedSizeError", "TransformMatrix",
     "VARIANTS", "digest", "expand_seed", "hash_bytes", "instance_count", "seed_for_input", "seed_layout",
     "seed_words_needed", "variant", "hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes",
-    "hash_fixed_folds", "hash_words_many_seeds", "StreamHasher", "varlen_status", "release_host", "ENGINES",
+    "hash_fixed_folds", "hash_words_many_seeds", "StreamHasher", "varlen_status", "release_host", "fill_strings", "ENGINES",
     "SUPPORTED_COEFFICIENTS", "coefficient_multiply",
     "__version__",
 ]
@@ -48,7 +48,7 @@ __all__ = [
 def __getattr__(name):
     # batch entry points import torch lazily so host-only use stays light
     if name in ("hash_fixed", "hash_varlen", "hash_words", "hash_fixed_host", "fill_bytes", "hash_fixed_folds",
-                "hash_words_many_seeds", "varlen_status", "release_host"):
+                "hash_words_many_seeds", "varlen_status", "release_host", "fill_strings"):
         from . import batch
 
         return getattr(batch, name)

@@ -25,8 +25,11 @@ EXPORTS = (
     "hth_hash_varlen", "hth_varlen_status", "hth_hash_host", "hth_hash_fixed_host",
     "hth_slice_plan", "hth_workspace_size_slice", "hth_hash_slice", "hth_hash_merge", "hth_hash_fixed_folds",
     "hth_ipc_get_handle", "hth_ipc_open_handle", "hth_ipc_close_handle", "hth_host_release",
-    "hth_workspace_reset",
+    "hth_workspace_reset", "hth_hash_slice_ex", "hth_hash_merge_ex", "hth_signal", "hth_wait_flag",
+    "hth_fill_splitmix_strings",
 )
+
+HTH_SLICE_ACCUMULATE = 1
 
 #: seed_capacity sentinel of the host entry points (HTH_SEED_AUTO)
 SEED_AUTO = (1 << 64) - 1
@@ -77,6 +80,11 @@ def lib() -> ctypes.CDLL:
             "hth_ipc_close_handle": [vp],
             "hth_host_release": [],
             "hth_workspace_reset": [vp, u64, vp],
+            "hth_hash_slice_ex": [i32, vp, u64, u64, u64, i32, u64, vp, u64, vp, vp, vp, u64, i32, vp, u64, vp],
+            "hth_hash_merge_ex": [i32, u64, i32, vp, u64, vp, u64, vp, u64, vp, vp, u64, vp, u64, vp, vp, u64, vp],
+            "hth_signal": [vp, u64, vp],
+            "hth_wait_flag": [vp, u64, u64, vp, vp],
+            "hth_fill_splitmix_strings": [u64, u64, u64, u64, u64, vp, u64, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)

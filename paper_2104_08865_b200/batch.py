@@ -20,7 +20,8 @@ from .hasher import SeedBuffer, _check_capacity, _check_params, seed_words_neede
 from .params import HashParams
 
 __all__ = ["hash_fixed", "hash_varlen", "varlen_status", "hash_words", "hash_fixed_host", "fill_bytes",
-           "workspace_fixed", "workspace_varlen", "hash_fixed_folds", "hash_words_many_seeds", "release_host"]
+           "workspace_fixed", "workspace_varlen", "hash_fixed_folds", "hash_words_many_seeds", "release_host",
+           "fill_strings"]
 
 
 def _stream(dev) -> int:
@@ -293,3 +294,20 @@ def fill_bytes(n_bytes: int, fill_seed: int = 0x243F6A8885A308D3, word_offset: i
 def release_host() -> None:
     """Free the calling thread's host-path streams and buffers (``hth_host_release``)."""
     _lib.check(_lib.lib().hth_host_release())
+
+
+def fill_strings(n_strings: int, n_bytes: int, first: int = 0, step: int = 1, fill_seed: int = 0x243F6A8885A308D3,
+                 out: torch.Tensor = None, stride: int = None, device=None) -> torch.Tensor:
+    """One launch: local string i = global string ``first + i * step`` of the
+    packed ``fill_bytes`` stream of ``n_bytes``-strings (a round-robin or
+    blocked shard of a batch; ``n_bytes % 8 == 0``)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+    stride = n_bytes if stride is None else stride
+    if out is None:
+        out = torch.empty(max(n_strings * stride, 16), dtype=torch.uint8, device=dev)
+    if n_strings and (n_strings - 1) * stride + n_bytes > out.numel():
+        raise ValueError("output tensor too small")
+    with torch.cuda.device(out.device):
+        _lib.check(_lib.lib().hth_fill_splitmix_strings(_u64(fill_seed), n_strings, n_bytes, first, step,
+                                                        out.data_ptr(), stride, _stream(out.device)))
+    return out

@@ -123,6 +123,33 @@ __device__ __forceinline__ u32 atom_add_acq_rel(u32* p, u32 v) {
   return old;
 }
 
+// System-scope release store / acquire load of a 64-bit flag (peer GPUs
+// over NVLink read and write these).
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, u64 v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_acquire_sys(const unsigned long long* p) {
+  u64 v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 global_ns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *p >= v, or give up after timeout_ns (returns false): a wait on
+// another GPU must never hang this one.
+__device__ __forceinline__ bool wait_geq_sys(const unsigned long long* p, u64 v, u64 timeout_ns) {
+  if (ld_acquire_sys(p) >= v) return true;
+  const u64 t0 = global_ns();
+  for (;;) {
+    __nanosleep(128);
+    if (ld_acquire_sys(p) >= v) return true;
+    if (global_ns() - t0 > timeout_ns) return false;
+  }
+}
+
 template <class T>
 __device__ __forceinline__ T shfl_xor(T v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
@@ -268,6 +295,11 @@ struct Params {
   u64 slice_job0;    // global jq of the slice's first job
   u64 frontier_base;
   u64* frontier;
+  // slice mode, in-stream exchange: the last warp out stores done_value to
+  // *done_flag (system-scope release; the flag may live on another GPU)
+  // after every warp's frontier/partial stores are visible system-wide
+  unsigned long long* done_flag;
+  u64 done_value;
   // EHC seed words S[0..e*w), split into halves.  The kernel takes Params as
   // a __grid_constant__, so these are constant-bank operands of the NH adds.
   // Interleaved (lo, hi), word i at slot ehc_slot(i): the leaf's block-u pass

@@ -166,6 +166,25 @@ __global__ void expand_seed_kernel(u64 fold, u64 start, u64 count, u64* out) {
     out[i] = mix64(fold + (start + i + 1) * 0x9E3779B97F4A7C15ull);
 }
 
+// Publish / await one flag in-stream (system scope; see wait_geq_sys).
+__global__ void signal_kernel(unsigned long long* flag, u64 value) {
+  __threadfence_system();
+  st_release_sys(flag, value);
+}
+__global__ void wait_kernel(const unsigned long long* flag, u64 value, u64 timeout_ns, int* status) {
+  if (!wait_geq_sys(flag, value, timeout_ns)) atomicExch(status, 1);
+  __threadfence_system();
+}
+
+// string i of a local buffer = global string first + i * step of a packed
+// stream of `wps`-word strings (round-robin shards in one launch)
+__global__ void fill_strings_kernel(u64 seed, u64 wps, u64 first, u64 step, u64 n_words, u64 dst_wstride, u64* dst) {
+  for (u64 w = blockIdx.x * (u64)blockDim.x + threadIdx.x; w < n_words; w += (u64)gridDim.x * blockDim.x) {
+    const u64 i = w / wps, t = w - i * wps;
+    dst[i * dst_wstride + t] = mix64(seed + ((first + i * step) * wps + t + 1) * 0x9E3779B97F4A7C15ull);
+  }
+}
+
 __global__ void fill_kernel(u64 seed, u64 woff, u64 n_words, u64 n_bytes, u64* dst) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n_words; i += (u64)gridDim.x * blockDim.x) {
     u64 v = mix64(seed + (woff + i + 1) * 0x9E3779B97F4A7C15ull);
@@ -545,6 +564,20 @@ int hth_fill_splitmix(uint64_t fill_seed, uint64_t word_offset, uint64_t n_bytes
   return HTH_OK;
 }
 
+int hth_fill_splitmix_strings(uint64_t fill_seed, uint64_t n_strings, uint64_t n_bytes, uint64_t first_string,
+                              uint64_t string_step, void* d_dst, uint64_t dst_stride, void* stream) {
+  if (!n_strings || !n_bytes) return HTH_OK;
+  if (n_bytes % 8 || dst_stride % 8 || dst_stride < n_bytes || !d_dst || (reinterpret_cast<uintptr_t>(d_dst) & 7))
+    return fail(HTH_EINVAL, "strided fill needs n_bytes, dst_stride and d_dst 8-byte aligned, dst_stride >= n_bytes");
+  const u64 nw = n_strings * (n_bytes / 8);
+  const u64 blocks = std::min<u64>(ceil_div(nw, 256), 148 * 64);
+  fill_strings_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(fill_seed, n_bytes / 8, first_string,
+                                                                          string_step, nw, dst_stride / 8,
+                                                                          (u64*)d_dst);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+
 int hth_workspace_size_fixed(int output_bytes, uint64_t n_strings, uint64_t n_bytes, uint64_t* bytes) {
   VarInfo v;
   if (int rc = get_var(output_bytes, &v)) return rc;
@@ -825,13 +858,14 @@ int hth_ipc_close_handle(void* d_ptr) {
   return HTH_OK;
 }
 
-int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
-                   int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
-                   uint64_t* d_frontier, uint64_t* d_partial, void* d_workspace, uint64_t workspace_bytes,
-                   void* stream) {
+static int slice_impl(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
+                      int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
+                      uint64_t* d_frontier, uint64_t* d_partial, uint64_t* d_done_flag, uint64_t done_value,
+                      int options, void* d_workspace, uint64_t workspace_bytes, void* stream) {
   VarInfo v;
   if (int rc = get_var(output_bytes, &v)) return rc;
   if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
+  if (options & ~HTH_SLICE_ACCUMULATE) return fail(HTH_EINVAL, "unknown slice options %d", options);
   const FixedPlan f = fixed_plan(v, 1, n_bytes, std::max(frontier_level, 1));
   const u64 per = 1ull << (3 * f.job_lvl), sub = 1ull << (3 * frontier_level);
   if (frontier_level < f.job_lvl || inst_begin % sub || inst_begin > inst_end || inst_end > f.n_inst ||
@@ -840,11 +874,17 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   if (!d_partial || !d_seed) return fail(HTH_EINVAL, "null device pointer");
   if (workspace_bytes < f.ws_total) return fail(HTH_EINVAL, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaMemsetAsync(d_partial, 0, v.k * 8, st));
+  if (!(options & HTH_SLICE_ACCUMULATE)) CK(cudaMemsetAsync(d_partial, 0, v.k * 8, st));
   const bool last = inst_end == f.n_inst;
   const u64 j0 = inst_begin / per;
   const u64 j1 = last ? f.J : inst_end / per;
-  if (j1 <= j0) return HTH_OK;
+  if (j1 <= j0) {  // nothing to hash: still publish the (empty) slice
+    if (d_done_flag) {
+      signal_kernel<<<1, 1, 0, st>>>(reinterpret_cast<unsigned long long*>(d_done_flag), done_value);
+      CK(cudaGetLastError());
+    }
+    return HTH_OK;
+  }
   const u64 byte0 = inst_begin * (u64)v.m * 8;
   Params P{};
   P.data = (const uint8_t*)d_slice - byte0;  // global byte b of the string lives at d_slice[b - byte0]
@@ -862,6 +902,8 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   P.slice_job0 = j0;
   P.frontier_base = inst_begin >> (3 * frontier_level);
   P.frontier = d_frontier;
+  P.done_flag = reinterpret_cast<unsigned long long*>(d_done_flag);
+  P.done_value = done_value;
   fill_ehc(v, seed_fold, P);
   fill_fin_const(v, seed_fold, n_bytes, P);
   uint8_t* ws = (uint8_t*)d_workspace;
@@ -873,14 +915,31 @@ int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint
   return guard_ws(dispatch<false>(output_bytes, P, P.n_jobs, st), d_workspace, f.ws_total, st);
 }
 
-int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
-                   uint64_t n_frontier, const uint64_t* d_partials, uint64_t n_partials, uint64_t seed_fold,
-                   const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out, void* d_workspace,
-                   uint64_t workspace_bytes, void* stream) {
+int hth_hash_slice(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
+                   int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
+                   uint64_t* d_frontier, uint64_t* d_partial, void* d_workspace, uint64_t workspace_bytes,
+                   void* stream) {
+  return slice_impl(output_bytes, d_slice, n_bytes, inst_begin, inst_end, frontier_level, seed_fold, d_seed,
+                    seed_capacity, d_frontier, d_partial, nullptr, 0, 0, d_workspace, workspace_bytes, stream);
+}
+
+int hth_hash_slice_ex(int output_bytes, const void* d_slice, uint64_t n_bytes, uint64_t inst_begin, uint64_t inst_end,
+                      int frontier_level, uint64_t seed_fold, const uint64_t* d_seed, uint64_t seed_capacity,
+                      uint64_t* d_frontier, uint64_t* d_partial, uint64_t* d_done_flag, uint64_t done_value,
+                      int options, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  return slice_impl(output_bytes, d_slice, n_bytes, inst_begin, inst_end, frontier_level, seed_fold, d_seed,
+                    seed_capacity, d_frontier, d_partial, d_done_flag, done_value, options, d_workspace,
+                    workspace_bytes, stream);
+}
+
+static int merge_impl(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
+                      uint64_t n_frontier, const uint64_t* d_partials, uint64_t n_partials, const uint64_t* d_seed,
+                      uint64_t seed_capacity, uint64_t* d_out, const uint64_t* d_flags, uint64_t epoch,
+                      uint64_t* d_consumed, uint64_t timeout_ns, int* d_status, void* d_workspace,
+                      uint64_t workspace_bytes, void* stream) {
   VarInfo v;
   if (int rc = get_var(output_bytes, &v)) return rc;
   if (int rc = check_seed(v, n_bytes, seed_capacity)) return rc;
-  (void)seed_fold;
   const u64 n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
   const u64 keep = (n_inst >> (3 * frontier_level)) & ~7ull;
   if (n_frontier != keep)
@@ -888,6 +947,7 @@ int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const
                 (unsigned long long)keep);
   const u64 need = 2 * (n_frontier / 8 + 8) * 8ull * v.k * 8;
   if (workspace_bytes < need) return fail(HTH_EINVAL, "merge workspace too small: need %llu", (unsigned long long)need);
+  if (d_flags && (!d_consumed || !d_status)) return fail(HTH_EINVAL, "flags need a consumed flag and a status word");
   MergeParams M{};
   M.n_bytes = n_bytes;
   M.c = frontier_level;
@@ -898,8 +958,49 @@ int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const
   M.S = d_seed;
   M.tmp = (u64*)d_workspace;
   M.out = d_out;
-  cudaStream_t st = (cudaStream_t)stream;
-  return by_width<MergeF>(output_bytes, M, st);
+  M.flags = reinterpret_cast<const unsigned long long*>(d_flags);
+  M.nflags = d_flags ? n_partials : 0;
+  M.epoch = epoch;
+  M.timeout_ns = timeout_ns;
+  M.consumed = reinterpret_cast<unsigned long long*>(d_consumed);
+  M.partials_rw = d_flags ? const_cast<u64*>(d_partials) : nullptr;
+  M.status = d_status;
+  return by_width<MergeF>(output_bytes, M, (cudaStream_t)stream);
+}
+
+int hth_hash_merge(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
+                   uint64_t n_frontier, const uint64_t* d_partials, uint64_t n_partials, uint64_t seed_fold,
+                   const uint64_t* d_seed, uint64_t seed_capacity, uint64_t* d_out, void* d_workspace,
+                   uint64_t workspace_bytes, void* stream) {
+  (void)seed_fold;
+  return merge_impl(output_bytes, n_bytes, frontier_level, d_frontier, n_frontier, d_partials, n_partials, d_seed,
+                    seed_capacity, d_out, nullptr, 0, nullptr, 0, nullptr, d_workspace, workspace_bytes, stream);
+}
+
+int hth_hash_merge_ex(int output_bytes, uint64_t n_bytes, int frontier_level, const uint64_t* d_frontier,
+                      uint64_t n_frontier, uint64_t* d_partials, uint64_t n_partials, const uint64_t* d_seed,
+                      uint64_t seed_capacity, uint64_t* d_out, const uint64_t* d_flags, uint64_t epoch,
+                      uint64_t* d_consumed, uint64_t timeout_ns, int* d_status, void* d_workspace,
+                      uint64_t workspace_bytes, void* stream) {
+  if (!d_flags) return fail(HTH_EINVAL, "hth_hash_merge_ex needs flags (use hth_hash_merge)");
+  return merge_impl(output_bytes, n_bytes, frontier_level, d_frontier, n_frontier, d_partials, n_partials, d_seed,
+                    seed_capacity, d_out, d_flags, epoch, d_consumed, timeout_ns, d_status, d_workspace,
+                    workspace_bytes, stream);
+}
+
+int hth_signal(uint64_t* d_flag, uint64_t value, void* stream) {
+  if (!d_flag) return fail(HTH_EINVAL, "null flag");
+  signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long*>(d_flag), value);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+
+int hth_wait_flag(const uint64_t* d_flag, uint64_t value, uint64_t timeout_ns, int* d_status, void* stream) {
+  if (!d_flag || !d_status) return fail(HTH_EINVAL, "null flag or status");
+  wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long*>(d_flag), value,
+                                                 timeout_ns, d_status);
+  CK(cudaGetLastError());
+  return HTH_OK;
 }
 
 // Strings longer than kChunk from host memory: each is streamed in slices

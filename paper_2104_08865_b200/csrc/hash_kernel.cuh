@@ -701,13 +701,21 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // slice mode: the frontier roots and partial digest may live in another
   // GPU's memory (peer stores over NVLink); make them visible system-wide
   if (P.frontier_lvl) __threadfence_system();
+  __syncwarp();
   // every warp has stopped claiming; the last one out re-zeroes the counters
   // (relaxed is enough: each warp's last claim returned before it got here)
-  if (claims && lane == 0) {
+  // and, exchanging in-stream, publishes the slice: every warp fenced its
+  // peer stores (fence.sc.sys above) before its arrival, so a fence and a
+  // release store by the last arriver order them all before the flag
+  if ((claims || P.done_flag) && lane == 0) {
     const u32 old = atomicAdd(P.exit_ctr, 1u);
     if (old + 1 == gridDim.x * (u32)W) {
       *P.job_ctr = 0;
       *P.exit_ctr = 0;
+      if (P.done_flag) {
+        __threadfence_system();
+        st_release_sys(P.done_flag, P.done_value);
+      }
     }
   }
 }

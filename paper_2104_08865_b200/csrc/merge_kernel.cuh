@@ -20,6 +20,15 @@ struct MergeParams {
   const u64* S;
   u64* tmp;              // nf/8 * 8k words scratch (ping-pong half)
   u64* out;              // k words
+  // in-stream exchange (optional): wait until flags[0..nflags) >= epoch
+  // (stored by the slices' kernels, possibly on other GPUs), then merge,
+  // re-zero the partials for the slot's next use and release *consumed =
+  // epoch.  A wait longer than timeout_ns sets *status = 1 (no hang).
+  const unsigned long long* flags;
+  u64 nflags, epoch, timeout_ns;
+  unsigned long long* consumed;
+  u64* partials_rw;
+  int* status;
 };
 
 template <int OUT>
@@ -32,6 +41,12 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Merg
 #pragma unroll
   for (int r = 0; r < K; r++) fin[r] = 0;
   if (threadIdx.x < K) red[threadIdx.x] = 0;
+  if (P.flags) {
+    for (u64 i = threadIdx.x; i < P.nflags; i += blockDim.x)
+      if (!wait_geq_sys(P.flags + i, P.epoch, P.timeout_ns)) atomicExch(P.status, 1);
+    __syncthreads();
+    __threadfence_system();
+  }
   const u64* cur = P.frontier;
   u64* bufs[2] = {P.tmp, P.tmp + (P.nf / 8 + 8) * 8 * K};
   u64 nf = P.nf;
@@ -45,9 +60,10 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Merg
       const int r = (int)((it / 8) % K), j = (int)(it % 8);
       const u64* blk = cur + g * 8 * 8 * K + r * 8 + j;
       const u64* s = P.S + (u64)EW + 7ull * L * r + 7ull * lvl;
-      u64 v = blk[7 * 8 * K];
+      // frontier blocks may have arrived from peer GPUs: read through L2
+      u64 v = __ldcg(blk + 7 * 8 * K);
 #pragma unroll
-      for (int q = 0; q < 7; q++) v = nh_acc(v, blk[q * 8 * K], __ldg(s + q));
+      for (int q = 0; q < 7; q++) v = nh_acc(v, __ldcg(blk + q * 8 * K), __ldg(s + q));
       if (g >= keep) {  // leftover at level lvl+1 -> finalize slot
         const u64 F = (u64)EW + 7ull * L * K + 64ull * L * r;
 #pragma unroll
@@ -69,8 +85,20 @@ __global__ void __launch_bounds__(256) merge_kernel(const __grid_constant__ Merg
   __syncthreads();
   if (threadIdx.x < K) {
     u64 v = red[threadIdx.x];
-    for (u64 p = 0; p < P.np; p++) v += P.partials[p * K + threadIdx.x];
+    for (u64 p = 0; p < P.np; p++) v += __ldcg(P.partials + p * K + threadIdx.x);
     P.out[threadIdx.x] = v;
+  }
+  if (P.flags) {
+    // the slot is consumed: zero its partials (the slices accumulate into
+    // them next time), then hand it back to the producers
+    __syncthreads();
+    if (P.partials_rw)
+      for (u64 i = threadIdx.x; i < P.np * K; i += blockDim.x) P.partials_rw[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(P.consumed, P.epoch);
+    }
   }
 }
 

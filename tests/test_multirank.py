@@ -106,3 +106,30 @@ def test_round_robin_shards_partition():
     assert np.array_equal(np.sort(seen), np.arange(n))
     blocks = [list(multi_gpu.shard_blocks(4194304, r, 8)) for r in range(8)]
     assert sum(len(b) for b in blocks) == 4194304
+
+
+def test_flag_exchange_slot_layout():
+    # rank 0's exchange buffer: two slots of [frontier | partials], then the
+    # arrival flags and consumed words, no overlaps, every rank's frontier
+    # range where the plan puts it
+    from paper_2104_08865_b200 import multi_gpu
+
+    for w, n, world in ((16, 16 << 30, 8), (40, 8 << 30, 3), (24, 5 << 20, 2)):
+        plan = multi_gpu.slice_plan(hh.variant(w), n, world)
+        lay = multi_gpu._SlotLayout(plan)
+        k = w // 8
+        spans = []
+        for slot in (0, 1):
+            for r in range(world):
+                a = lay.frontier(0, slot, r) // 8
+                spans.append((a, a + plan.counts[r] * 8 * k))
+                b = lay.partials(0, slot, r) // 8
+                spans.append((b, b + k))
+                f = lay.flag(0, slot, r) // 8
+                spans.append((f, f + 1))
+            c = lay.consumed(0, slot) // 8
+            spans.append((c, c + 1))
+        spans = sorted(s for s in spans if s[1] > s[0])
+        assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+        assert spans[-1][1] <= lay.words
+        assert sum(b - a for a, b in spans) == lay.words
