@@ -697,9 +697,12 @@ def arm_split(args, rank, world, local_rank, hh, torch, dist):
             "gpu_launches": (2 if exchange != "nccl" else 2) * args.steps,
             "clocks": sampler.summary(wall0, wall1),
             "ranks": ranks,
+            "ranks_share_gpu": not distinct,
             "comm": _comm(dist),
             "oracle_check": check,
         }
+        if not distinct:
+            line["note"] = "ranks share one GPU (multi-rank code path exercised; timings are not a scaling number)"
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
@@ -860,9 +863,11 @@ def arm_ours(args, rank, world, local_rank):
     ms = float(t.item()) / args.steps
     value = world * value_bytes / (ms / 1e3) / 1e9
     achieved = algo / (kernel_ms / 1e3) / 1e9
-    ranks = _rank_report(dist, {"rank": rank, "device": dev_name, "local_rank": local_rank,
+    uuid = str(getattr(torch.cuda.get_device_properties(local_rank), "uuid", local_rank))
+    ranks = _rank_report(dist, {"rank": rank, "device": dev_name, "uuid": uuid, "local_rank": local_rank,
                                 "busy_ms_per_step": total_ms / args.steps, "kernel_ms": kernel_ms,
                                 "clocks": clocks})
+    shared = len({r["uuid"] for r in ranks}) < len(ranks)
     e2e = None
     if args.e2e_steps > 0 and workload != "cfg2":
         try:
@@ -945,10 +950,13 @@ def arm_ours(args, rank, world, local_rank):
             "gpu_launches": args.steps * (8 if workload == "cfg2" else 1),
             "clocks": clocks,
             "ranks": ranks,
+            "ranks_share_gpu": shared,
             "comm": _comm(dist),
             "oracle_check": check,
             "workloads": extra,
         }
+        if shared:
+            line["note"] = "ranks share one GPU (multi-rank code path exercised; timings are not a scaling number)"
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
