@@ -95,12 +95,16 @@ inline int tail_cpt(u64 nch) {
 }
 template <int OUT, bool MASKED>
 int dispatch_tail_m(const TailParams& P, u64 nch, cudaStream_t st) {
+  // a string shorter than one instance has at most ceil((8m - 8) / 16)
+  // chunks: 48 (v16), 84 (v24/v32), 60 (v40) -- only v24/v32 need CPT 6
+  constexpr bool WIDE = Geo<Var<OUT>>::m * 8 - 8 > 16 * 16 * 4;
   switch (tail_cpt(nch)) {
     case 1: return launch_tail<OUT, 1, MASKED>(P, st);
     case 2: return launch_tail<OUT, 2, MASKED>(P, st);
     case 4: return launch_tail<OUT, 4, MASKED>(P, st);
   }
-  return launch_tail<OUT, 6, MASKED>(P, st);
+  if constexpr (WIDE) return launch_tail<OUT, 6, MASKED>(P, st);
+  return fail(HTH_EINVAL, "tail kernel: %llu chunks exceed one instance", (unsigned long long)nch);
 }
 template <int OUT>
 int dispatch_tail(const TailParams& P, u64 nch, cudaStream_t st) {

@@ -97,7 +97,6 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
   // Toeplitz keys for this lane's chunks: chunk c covers words 2c, 2c+1 and
   // needs S[R + 2c + r] for r <= K
   u32 klo[CPT][K + 1], khi[CPT][K + 1];
-  u64 mask0[CPT], mask1[CPT];  // zero-padding / words past the end (MASKED only)
 #pragma unroll
   for (int i = 0; i < CPT; i++) {
     const u32 c = (u32)g + 16u * i;
@@ -107,10 +106,13 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
       klo[i][r] = (u32)s;
       khi[i][r] = (u32)(s >> 32);
     }
-    const u64 b0 = 16ull * c, b1 = b0 + 8;
-    mask0[i] = b0 >= n ? 0 : (b0 + 8 <= n ? ~0ull : (1ull << (8 * (n - b0))) - 1);
-    mask1[i] = b1 >= n ? 0 : (b1 + 8 <= n ? ~0ull : (1ull << (8 * (n - b1))) - 1);
   }
+  // MASKED: only the string's last chunk can be partial (chunks past it are
+  // skipped), so two masks serve every lane: zero-padding of the final word
+  // (hasher.py:179-183) and the word past the end
+  const u64 lb0 = 16ull * (nch - 1), lb1 = lb0 + 8;
+  const u64 lmask0 = lb0 + 8 <= n ? ~0ull : (1ull << (8 * (n - lb0))) - 1;
+  const u64 lmask1 = lb1 >= n ? 0 : (lb1 + 8 <= n ? ~0ull : (1ull << (8 * (n - lb1))) - 1);
   const u64 NW = (u64)gridDim.x * (blockDim.x >> 5);
   const u64 w0 = (u64)blockIdx.x * (blockDim.x >> 5) + warp;
   const u64 pairs = (P.n_strings + 1) >> 1;
@@ -163,9 +165,9 @@ __global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ Ta
         const u32 c = (u32)g + 16u * i;
         if (!MASKED || c < nch) {
           w2 x0 = {v[i].x, v[i].y}, x1 = {v[i].z, v[i].w};
-          if (MASKED) {
-            x0 = mk((((u64)v[i].y << 32) | v[i].x) & mask0[i]);
-            x1 = mk((((u64)v[i].w << 32) | v[i].z) & mask1[i]);
+          if (MASKED && c == nch - 1) {
+            x0 = mk((((u64)v[i].y << 32) | v[i].x) & lmask0);
+            x1 = mk((((u64)v[i].w << 32) | v[i].z) & lmask1);
           }
           const bool w1 = !MASKED || 2 * c + 1 < nw;
 #pragma unroll

@@ -378,6 +378,15 @@ def test_config5_full_16gib(hh):
     want = coracle.hash_huge(16, host, seed.words_np(0, seed.capacity))
     assert np.array_equal(full, want)
     assert np.array_equal(sliced, want)
+    # and the digest the reference itself produced for this string
+    # (tests/golden/deep_vectors.jsonl, chunked harness over its internals)
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "deep_vectors.jsonl")) as fh:
+        ref = [r for r in map(json.loads, fh) if r["kind"] == "huge"][0]
+    assert ref["length"] == n and bytes.fromhex(ref["master"]) == MASTER
+    assert full.tobytes().hex() == ref["digest"]
 
 
 # ------------------------------------------------------------------ many seeds

@@ -3,6 +3,8 @@
 CPU only.  The oracle is the checker for every GPU parity test, so it must
 reproduce the reference bit for bit first."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -89,3 +91,22 @@ def test_seed_stream_and_layout():
     for w in (16, 24, 32, 40):
         for n in (0, 1, 1000, 10 ** 6, 16 << 30):
             assert coracle.seed_words_needed(w, n) == o.seed_words_needed(o.variant(w), n)
+
+
+def test_oracle_matches_reference_deep_trees():
+    # L = 6 and 7 records the reference computed (tests/golden/deep_vectors.jsonl)
+    import json
+
+    from oracle import c as coracle
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "deep_vectors.jsonl")
+    with open(path) as fh:
+        recs = [r for r in map(json.loads, fh) if r["kind"] == "deep" and r["levels"] <= 7]
+    assert len(recs) == 8
+    for r in recs:
+        n = r["length"]
+        kind, seed, off = r["generator"].split(":")
+        host = coracle.splitmix(int(seed, 16), int(off), (n + 7) // 8).view(np.uint8)[:n].copy()
+        S = o.splitmix_words(o.master_fold(bytes.fromhex(r["master"])), 0, o.seed_words_needed(o.variant(r["variant"]), n))
+        got = coracle.hash_huge(r["variant"], host, S)
+        assert got.tobytes().hex() == r["digest"], (r["variant"], r["levels"])

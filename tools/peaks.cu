@@ -3,6 +3,12 @@
 //   copy   -- HBM read + write (the MEASURED_PEAKS.json figure's kind)
 //   imad   -- IMAD.WIDE.U32 issue rate (the NH multiply)
 //   lop3   -- 3-input LOP3 issue rate (the GF(16) encode)
+//   tma    -- HBM read-only streaming through cp.async.bulk into a per-warp
+//             shared-memory ring (the hash kernels' load path), best of a
+//             sweep over stage size and warps per SM
+//   floor  -- config 1's shape (1024 warps x 4 KiB after an L2 flush): an
+//             empty launch, one bulk copy + 24-byte store per warp, and the
+//             same with LDG.128 loads, each timed by events around the launch
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/peaks tools/peaks.cu
 // Run:   tools/peaks > profiles/peaks.json      (one GPU; prints one JSON object)
 #include <cstdint>
@@ -66,6 +72,98 @@ __global__ void lop3_kernel(uint32_t a, int iters, uint32_t* sink) {
   if (s == 1) sink[0] = s;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Each warp streams chunks w, w + W, ... of `stage` bytes through an NS-slot
+// ring; lane 0 issues, all lanes read one word per chunk (as a consumer would).
+template <int NS>
+__global__ void tma_read_kernel(const uint8_t* __restrict__ p, size_t bytes, uint32_t stage, uint32_t* sink) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  uint8_t* ring = smem + (size_t)warp * NS * stage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)wpb * NS * stage) + warp * NS;
+  if (lane == 0) {
+    for (int i = 0; i < NS; i++) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const size_t nchunks = bytes / stage, W = (size_t)gridDim.x * wpb;
+  size_t next = blockIdx.x * (size_t)wpb + warp;
+  uint32_t pseq = 0, acc = 0;
+  for (int i = 0; i < NS && next < nchunks; i++, next += W, pseq++) {
+    if (lane == 0) {
+      mbar_expect(&bars[i], stage);
+      bulk_g2s(ring + i * stage, p + next * stage, stage, &bars[i]);
+    }
+  }
+  for (uint32_t c = 0; c < pseq; c++) {
+    const uint32_t slot = c % NS;
+    mbar_wait(&bars[slot], (c / NS) & 1);
+    acc ^= reinterpret_cast<const uint32_t*>(ring + slot * stage)[lane];
+    __syncwarp();
+    if (next < nchunks) {
+      if (lane == 0) {
+        mbar_expect(&bars[slot], stage);
+        bulk_g2s(ring + slot * stage, p + next * stage, stage, &bars[slot]);
+      }
+      next += W;
+      pseq++;
+    }
+  }
+  if (acc == 0x9E3779B9u) sink[0] = acc;
+}
+
+__global__ void empty_kernel() {}
+
+// config 1's shape: warp w reads string w (4 KiB) -- by one bulk copy or by
+// LDG.128 -- and stores 24 bytes
+__global__ void floor_tma_kernel(const uint8_t* __restrict__ p, uint32_t n, uint64_t* out) {
+  __shared__ __align__(128) uint8_t buf[2][4096];
+  __shared__ uint64_t bar[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t s = blockIdx.x * (size_t)(blockDim.x >> 5) + warp;
+  if (lane == 0) {
+    mbar_init(&bar[warp], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect(&bar[warp], n);
+    bulk_g2s(buf[warp], p + s * n, n, &bar[warp]);
+  }
+  __syncwarp();
+  mbar_wait(&bar[warp], 0);
+  uint64_t v = reinterpret_cast<const uint64_t*>(buf[warp])[lane];
+  for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  if (lane < 3) out[s * 3 + lane] = v + lane;
+}
+__global__ void floor_ldg_kernel(const uint4* __restrict__ p, uint32_t n, uint64_t* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t s = blockIdx.x * (size_t)(blockDim.x >> 5) + warp;
+  const uint4* q = p + s * (n / 16);
+  uint32_t acc = 0;
+  for (uint32_t i = lane; i < n / 16; i += 32) {
+    const uint4 v = __ldcs(q + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  uint64_t v = acc;
+  for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  if (lane < 3) out[s * 3 + lane] = v + lane;
+}
+
 template <class F>
 float time_ms(F launch, int reps) {
   cudaEvent_t e0, e1;
@@ -101,12 +199,62 @@ int main() {
   const float im = time_ms([&] { imad_kernel<<<sms * 16, 256>>>(3, 5, iters, (uint64_t*)sink); }, 5);
   const float lo = time_ms([&] { lop3_kernel<<<sms * 16, 256>>>(7, iters, sink); }, 5);
   CK(cudaGetLastError());
+  // TMA bulk-copy read sweep: stage bytes x warps per SM (2-slot ring per warp)
+  float best_tma = 1e30f;
+  int best_stage = 0, best_wps = 0;
+  for (uint32_t stage : {4096u, 8192u, 16384u}) {
+    for (int wps : {8, 12, 16, 24}) {
+      const int wpb = 4, ctas = sms * wps / wpb;
+      const size_t smem = (size_t)wpb * 2 * stage + wpb * 2 * 8;
+      if (smem * (wps / wpb) > 220 * 1024) continue;
+      CK(cudaFuncSetAttribute(tma_read_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const float t = time_ms([&] { tma_read_kernel<2><<<ctas, wpb * 32, smem>>>((const uint8_t*)a, bytes, stage, sink); }, 10);
+      if (t < best_tma) {
+        best_tma = t;
+        best_stage = (int)stage;
+        best_wps = wps;
+      }
+    }
+  }
+  CK(cudaGetLastError());
+  // config-1 floor: flush L2 (256 MB write), then event / launch / event
+  uint8_t* flush = nullptr;
+  uint64_t* out = nullptr;
+  CK(cudaMalloc(&flush, 256u << 20));
+  CK(cudaMalloc(&out, 1024 * 3 * 8));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto floor = [&](auto launch) {
+    float sum = 0;
+    for (int r = 0; r < 21; r++) {
+      cudaMemsetAsync(flush, r, 256u << 20);
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r) sum += ms;
+    }
+    return sum / 20 * 1000.0f;  // us
+  };
+  const float f_empty = floor([&] { empty_kernel<<<512, 64>>>(); });
+  const float f_tma = floor([&] { floor_tma_kernel<<<512, 64>>>((const uint8_t*)a, 4096, out); });
+  const float f_ldg = floor([&] { floor_ldg_kernel<<<512, 64>>>(a, 4096, out); });
+  CK(cudaGetLastError());
   const double ops = (double)sms * 16 * 256 * iters * 8;
   printf("{\"device_sms\": %d, \"clock_mhz_attr\": %d, \"read_gbs\": %.1f, \"copy_gbs\": %.1f, "
+         "\"tma_read_gbs\": %.1f, \"tma_read_best\": {\"stage_bytes\": %d, \"warps_per_sm\": %d}, "
          "\"imad_wide_per_clk_per_sm_at_attr_clock\": %.1f, \"lop3_per_clk_per_sm_at_attr_clock\": %.1f, "
-         "\"imad_wide_tops\": %.2f, \"lop3_tops\": %.2f, \"note\": \"read: ld.global.cs 16 B/thread over 8 GiB; "
-         "copy: 4 GiB read + 4 GiB written, GB/s counts both; op rates are thread-instructions per second\"}\n",
-         sms, clk / 1000, bytes / (rd * 1e6), bytes / (cp * 1e6), ops / (im * 1e-3) / sms / (clk * 1e3),
-         ops / (lo * 1e-3) / sms / (clk * 1e3), ops / (im * 1e-3) / 1e12, ops / (lo * 1e-3) / 1e12);
+         "\"imad_wide_tops\": %.2f, \"lop3_tops\": %.2f, "
+         "\"cfg1_floor_us\": {\"empty_launch\": %.2f, \"bulk_copy_4KiB_per_warp\": %.2f, \"ldg128_4KiB_per_warp\": %.2f}, "
+         "\"note\": \"read: ld.global.cs 16 B/thread over 8 GiB; tma: cp.async.bulk into a 2-slot ring per warp over "
+         "8 GiB, best of stage x warps/SM; copy: 4 GiB read + 4 GiB written, GB/s counts both; op rates are "
+         "thread-instructions per second; cfg1 floor: 512 CTAs x 2 warps (1024 x 4 KiB, 4 MiB) after a 256 MB "
+         "memset, CUDA events around the launch, mean of 20\"}\n",
+         sms, clk / 1000, bytes / (rd * 1e6), bytes / (cp * 1e6), bytes / (best_tma * 1e6), best_stage, best_wps,
+         ops / (im * 1e-3) / sms / (clk * 1e3), ops / (lo * 1e-3) / sms / (clk * 1e3), ops / (im * 1e-3) / 1e12,
+         ops / (lo * 1e-3) / 1e12, f_empty, f_tma, f_ldg);
   return 0;
 }
