@@ -1,6 +1,7 @@
 // libhalftime_b200.so: C-ABI of the B200-native HalftimeHash engine.
 // Declarations and error conventions: include/halftime_b200.h.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -330,6 +331,18 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPl
 // one-stream path through pinned staging: a single-string hash_bytes call is
 // then one H2D DMA, one launch, one D2H DMA and one synchronize
 constexpr u64 kSmallCall = 256 << 10, kSmallOut = 4096;
+// calls up to this many input bytes skip both DMAs: the kernel reads the
+// input straight out of mapped pinned host memory (over PCIe) and writes the
+// digest words back into it, so a hash_bytes call is one launch and one
+// synchronize (HTH_HOST_MAPPED=0 turns this off)
+constexpr u64 kMappedCall = 64 << 10;
+bool mapped_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HTH_HOST_MAPPED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 // larger calls move ~kChunk bytes per chunk; strings longer than kChunk are
 // streamed through the same bounded buffers in slices (hth_hash_slice), so
 // device memory stays at 3 chunks whatever the input size
@@ -347,8 +360,10 @@ struct HostCtx {
   u64 ws_bytes[3] = {0, 0, 0};
   // small-call path: pinned staging both ways, and the fold whose first
   // `seeds_valid` words are already expanded in `seeds`
-  uint8_t* hin = nullptr;
+  uint8_t* hin = nullptr;  // pinned and mapped: din / dout are their device addresses
   u64* hout = nullptr;
+  uint8_t* din = nullptr;
+  u64* dout = nullptr;
   u64 seeds_fold = 0, seeds_valid = 0;
   // pageable sources: two pinned staging slots filled by parallel memcpy
   uint8_t* ring[2] = {nullptr, nullptr};
@@ -421,8 +436,10 @@ int host_ctx(int device, HostCtx** out) {
     CK(cudaEventCreateWithFlags(&c.ev, cudaEventDisableTiming));
   }
   if (!c.hin) {
-    CK(cudaHostAlloc((void**)&c.hin, kSmallCall + 16, cudaHostAllocDefault));
-    CK(cudaHostAlloc((void**)&c.hout, kSmallOut * 8, cudaHostAllocDefault));
+    CK(cudaHostAlloc((void**)&c.hin, kSmallCall + 16, cudaHostAllocMapped));
+    CK(cudaHostAlloc((void**)&c.hout, kSmallOut * 8, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&c.din, c.hin, 0));
+    CK(cudaHostGetDevicePointer((void**)&c.dout, c.hout, 0));
   }
   *out = &c;
   return HTH_OK;
@@ -1098,6 +1115,15 @@ int hth_hash_fixed_host(int output_bytes, const void* h_data, uint64_t n_strings
   if (nchunks == 1 && in_bytes <= kSmallCall && n_strings * k <= kSmallOut) {
     cudaStream_t st = c->st[0];
     if (int rc = host_seeds(c, fold, lay.total, st)) return rc;
+    if (in_bytes <= kMappedCall && mapped_enabled()) {
+      if (in_bytes) std::memcpy(c->hin, h_data, in_bytes);
+      if (int rc = hth_hash_fixed(output_bytes, c->din, n_strings, dstride, n_bytes, fold, c->seeds, lay.total,
+                                  c->dout, c->ws[0], c->ws_bytes[0], st))
+        return rc;
+      CK(cudaStreamSynchronize(st));
+      std::memcpy(h_out, c->hout, n_strings * k * 8);
+      return HTH_OK;
+    }
     if (in_bytes) {
       std::memcpy(c->hin, h_data, in_bytes);
       CK(cudaMemcpyAsync(c->buf[0], c->hin, in_bytes, cudaMemcpyHostToDevice, st));

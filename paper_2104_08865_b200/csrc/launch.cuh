@@ -172,7 +172,11 @@ int VarEngine<OUT>::plan(const PlanParams& Q, unsigned grid, cudaStream_t st) {
 }
 template <int OUT>
 int VarEngine<OUT>::merge(const MergeParams& M, cudaStream_t st) {
-  merge_kernel<OUT><<<1, 256, 0, st>>>(M);
+  auto kern = merge_kernel<OUT>;
+  const size_t smem = merge_smem_bytes<Var<OUT>::k>(M.nf);
+  int dev = 0, occ = 1;
+  if (int rc = occupancy((const void*)kern, MERGE_TPB, smem, &dev, &occ)) return rc;  // raises the smem limit
+  kern<<<1, MERGE_TPB, smem, st>>>(M);
   CK(cudaGetLastError());
   return HTH_OK;
 }
