@@ -32,9 +32,14 @@
  *    workspace zero-filled again (self-resetting counters/accumulators,
  *    consumed subtree blocks cleared), so it is reused across calls on one
  *    stream without clearing and the hot path is a single kernel launch.
- *    hth_hash_varlen clears its own state per call; a workspace it used must
- *    be re-zeroed before hth_hash_fixed uses it.  Concurrent calls need
- *    distinct workspaces.
+ *    hth_hash_varlen workspaces likewise: zero-filled before the first use;
+ *    the engine clears their counter region itself on the first call with
+ *    each batch layout (n_strings, total_bytes, variant) and otherwise relies
+ *    on the kernels leaving it zeroed, so a repeated batch shape is two
+ *    launches and no memset.  Do not write into a workspace between calls;
+ *    one that hth_hash_varlen used must be re-zeroed (hth_workspace_reset)
+ *    before hth_hash_fixed uses it.  Concurrent calls need distinct
+ *    workspaces.
  *  - Seeds (SeedBuffer, hasher.py:70-102): seed_fold is the master fold
  *    (hth_master_fold) and d_seed holds its expansion S[0..seed_capacity)
  *    (hth_expand_seed(seed_fold, 0, seed_capacity, d_seed), i.e.
@@ -129,10 +134,11 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
                     uint64_t max_n_bytes, uint64_t total_bytes, uint64_t seed_fold, const uint64_t* d_seed,
                     uint64_t seed_capacity, uint64_t* d_out, void* d_workspace, uint64_t workspace_bytes,
                     void* stream);
-/* Synchronizes `stream`; returns HTH_ESEEDSIZE if the last varlen call on this
- * workspace met a string longer than its max_n_bytes, HTH_EINVAL if offsets
- * decreased or ran past total_bytes, else HTH_OK (the reference raises
- * SeedSizeError / ValueError for these, hasher.py:209-214). */
+/* Synchronizes `stream`; returns HTH_ESEEDSIZE if a varlen call on this
+ * workspace since the previous status read met a string longer than its
+ * max_n_bytes, HTH_EINVAL if offsets decreased or ran past total_bytes, else
+ * HTH_OK (the reference raises SeedSizeError / ValueError for these,
+ * hasher.py:209-214).  Reading clears the flags. */
 int hth_varlen_status(void* d_workspace, void* stream);
 
 /* Re-zero a workspace (stream-ordered).  The device entry points already do

@@ -88,7 +88,7 @@ def _call(cache, dev, rc_fn):
 
 
 _WS = _Workspace()       # hash_fixed: zero-filled, kept zero by the engine
-_WS_VAR = _Workspace()   # hash_varlen: plan areas are scratch, cleared per call
+_WS_VAR = _Workspace()   # hash_varlen: zero-filled; the engine clears it per batch layout
 
 
 def hash_fixed(data: torch.Tensor, n_bytes: int, seed, params: HashParams, n_strings: int = None,

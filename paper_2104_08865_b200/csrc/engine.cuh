@@ -160,6 +160,104 @@ __device__ __forceinline__ u64 warp_sum(u64 v) {
   return v;
 }
 
+// Sum v[0..K) over the 16 lanes of each half-warp; afterwards lane g holds
+// the total of word (g & (KP-1)) for g < KP (KP = K rounded up to 2^n).
+template <int K>
+__device__ __forceinline__ u64 half_reduce_scatter(u64 (&v)[K], int g) {
+  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
+  u64 a[KP];
+#pragma unroll
+  for (int r = 0; r < KP; r++) a[r] = r < K ? v[r] : 0;
+  // step with mask 8 (and 4 when KP == 8): halve the live words per lane
+  int live = KP;
+#pragma unroll
+  for (int m = 8; m >= 1; m >>= 1) {
+    if (live > 1) {
+      const int half = live / 2;
+      const bool upper = (g & m) != 0;  // keep upper half of the live words
+#pragma unroll
+      for (int r = 0; r < KP / 2; r++) {
+        if (r < half) {
+          const u64 send = upper ? a[r] : a[r + half];
+          const u64 keep = upper ? a[r + half] : a[r];
+          a[r] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+      }
+      live = half;
+    } else {
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], m);
+    }
+  }
+  return a[0];
+}
+
+// lane g ends with the word index it holds after half_reduce_scatter
+template <int K>
+__device__ __forceinline__ int scatter_index(int g) {
+  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
+  int idx = 0, live = KP;
+  for (int m = 8; m >= 1 && live > 1; m >>= 1) {
+    const int half = live / 2;
+    if (g & m) idx += half;
+    live = half;
+  }
+  return idx;
+}
+
+// Sum NP values over all 32 lanes, scattered: afterwards every lane holds
+// the total of value warp_scatter_index<NP>(lane) (lanes differing only in
+// bits below 32 / NP hold the same one).  5 + NP - 2 shuffle rounds instead
+// of 5 per value.
+template <int NP>
+__device__ __forceinline__ u64 warp_reduce_scatter(u64 (&a)[NP], int lane) {
+  int live = NP;
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    if (live > 1) {
+      const int half = live / 2;
+      const bool upper = (lane & m) != 0;
+#pragma unroll
+      for (int r = 0; r < NP / 2; r++) {
+        if (r < half) {
+          const u64 send = upper ? a[r] : a[r + half];
+          const u64 keep = upper ? a[r + half] : a[r];
+          a[r] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+      }
+      live = half;
+    } else {
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], m);
+    }
+  }
+  return a[0];
+}
+template <int NP>
+__device__ __forceinline__ int warp_scatter_index(int lane) {
+  int idx = 0, live = NP;
+#pragma unroll
+  for (int m = 16; m >= 1 && live > 1; m >>= 1) {
+    const int half = live / 2;
+    if (lane & m) idx += half;
+    live = half;
+  }
+  return idx;
+}
+
+// Little-endian u64 word t of the string at byte `o0` of `data` (n bytes),
+// straight from global memory at any alignment, the partial last word
+// zero-padded (hasher.py:179-183); never reads past the string's last byte's
+// aligned word.
+__device__ __forceinline__ u64 gword(const uint8_t* data, u64 o0, u64 n, u64 t) {
+  const u64 b = reinterpret_cast<u64>(data) + o0 + 8ull * t;
+  const u64* p = reinterpret_cast<const u64*>(b & ~7ull);
+  const u32 sh = (u32)(b & 7) * 8;
+  const u64 rem = n - 8ull * t;
+  u64 x = __ldg(p) >> sh;
+  if (sh && rem > 8 - (b & 7)) x |= __ldg(p + 1) << (64 - sh);
+  if (rem < 8) x &= (1ull << (8 * rem)) - 1;
+  return x;
+}
+
 // splitmix seed word idx of a stream keyed by `fold` (hasher.py:55-58)
 __host__ __device__ __forceinline__ u64 splitmix_word(u64 fold, u64 idx) {
   u64 z = fold + (idx + 1) * 0x9E3779B97F4A7C15ull;
@@ -243,9 +341,19 @@ __host__ __device__ __forceinline__ u32 string_events(u64 n_inst, int job_lvl) {
 // Varlen jobs are bucketed by size class c = min(instances, 64) into queues
 // of fixed capacity: a class-c job holds >= c instances, so at most
 // q_inst / c of them exist.  Claim order is largest class first (LPT).
+// Classes 1..PAIR_MAX hold single-job strings only (one level, c
+// instances): the hash kernel takes them two per round.  A multi-job
+// string's last job of <= PAIR_MAX instances goes to class PAIR_MAX + 1
+// (at most one per 64 instances of the batch).
 constexpr int NCLS = 65;
+#ifndef HTH_PAIR_MAX
+#define HTH_PAIR_MAX 4
+#endif
+constexpr int PAIR_MAX = HTH_PAIR_MAX;  // 0: no pair jobs (experiments)
+static_assert(PAIR_MAX >= 0 && PAIR_MAX <= 4, "a pair's instances must fit one stage");
 __host__ __device__ __forceinline__ u64 queue_cap(int c, u64 max_jobs, u64 q_inst) {
-  return c == 0 ? 0 : min(max_jobs, q_inst / (u64)c + 1);
+  if (c == 0) return 0;
+  return min(max_jobs, q_inst / (u64)c + 1 + (c == PAIR_MAX + 1 ? q_inst / 64 + 1 : 0));
 }
 
 // Zero-slot finalize sums (tree.py:103-134): for a layout with L levels,
@@ -268,8 +376,9 @@ struct Params {
   const u64* offsets;  // varlen: n_strings + 1 byte offsets
   const u64* job_map;  // varlen: per-size-class job queues; each job a JOB_REC-word record
                        // {byte offset, length, string | job index << 32, 0} (plan_tail_kernel)
-  const u64* meta;     // varlen: 2 u64 per string (scratch, counter bases; multi-job strings)
-  const u32* cls_cnt;  // varlen: jobs per size class (plan_queue_kernel)
+  u32* cls_cnt;        // varlen: jobs per size class (plan_kernel; reset at exit)
+  unsigned long long* totals;  // varlen: the plan's scratch/counter allocators (reset at exit)
+  u64 var_total;       // varlen: data bytes (offset bound)
   const u64* ztab;     // varlen: zero-slot finalize sums per (levels, level, digit, row)
   u32 ztab_lmax;       // varlen: levels covered by ztab
   const u64* S;        // expanded seed words (SeedBuffer.words_np)
@@ -300,6 +409,9 @@ struct Params {
   // after every warp's frontier/partial stores are visible system-wide
   unsigned long long* done_flag;
   u64 done_value;
+#ifdef HTH_DEBUG_TIMING
+  unsigned long long* dbg;  // experiment builds: per-warp timing records (hth_debug_timing)
+#endif
   // EHC seed words S[0..e*w), split into halves.  The kernel takes Params as
   // a __grid_constant__, so these are constant-bank operands of the NH adds.
   // Interleaved (lo, hi), word i at slot ehc_slot(i): the leaf's block-u pass
@@ -358,9 +470,9 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, const u64* 
     st.L = P.L_fixed;
     st.J = (u32)P.J_fixed;
   }
-  if (VARLEN) {  // merge scratch and counters: multi-job strings only
-    st.scratch = st.J > 1 ? P.meta[2 * s] : 0;
-    st.cnt = st.J > 1 ? P.meta[2 * s + 1] : 0;
+  if (VARLEN) {  // merge scratch and counters (multi-job strings): packed in the record
+    st.scratch = rec[3] & ((1ull << 40) - 1);
+    st.cnt = rec[3] >> 40;
   }
 }
 

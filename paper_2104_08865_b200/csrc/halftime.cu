@@ -118,10 +118,21 @@ void fill_ehc(const VarInfo& v, u64 fold, Params& P) {
   }
 }
 
+#ifdef HTH_DEBUG_TIMING
+unsigned long long* dbg_buf() {
+  static unsigned long long* d = nullptr;
+  if (!d && cudaMalloc(&d, 8192 * 12 * 8) == cudaSuccess) cudaMemset(d, 0, 8192 * 12 * 8);
+  return d;
+}
+#endif
+
 // dynamic job-claim counter and exit counter (zero-filled, self-resetting)
 void set_ctl(Params& P, uint8_t* ctl) {
   P.job_ctr = reinterpret_cast<unsigned long long*>(ctl);
   P.exit_ctr = reinterpret_cast<u32*>(ctl + 8);
+#ifdef HTH_DEBUG_TIMING
+  P.dbg = dbg_buf();
+#endif
 }
 
 // Zero-slot + length-tag finalize terms of one string length, summed on the
@@ -247,6 +258,29 @@ int guard_ws(int rc, void* ws, u64 bytes, cudaStream_t st) {
   return rc;
 }
 
+// Varlen workspaces: the hash kernel leaves its counters, accumulators and
+// the plan's class counts zeroed, so a workspace reused with the same layout
+// needs no clearing; a layout change (another batch shape) may leave an
+// earlier call's T list / job records where this call's counters live, so
+// the counter region is cleared once, on the first call with each layout.
+struct WsSig {
+  u64 v[8];
+  bool operator==(const WsSig& o) const { return memcmp(v, o.v, sizeof v) == 0; }
+};
+std::mutex g_ws_mu;
+std::map<const void*, WsSig> g_ws_sig;
+bool ws_layout_known(const void* ws, const WsSig& sig) {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  auto it = g_ws_sig.find(ws);
+  if (it != g_ws_sig.end() && it->second == sig) return true;
+  g_ws_sig[ws] = sig;
+  return false;
+}
+void ws_forget(const void* ws) {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  g_ws_sig.erase(ws);
+}
+
 int check_seed(const VarInfo& v, u64 n_bytes, u64 cap) {
   const Layout l = make_layout(v, n_bytes);
   if (cap < l.total)
@@ -284,7 +318,7 @@ FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes, int frontier 
 
 // varlen workspace geometry
 struct VarPlan {
-  u64 off_err, off_cnt, off_acc, off_ev, off_ctl, off_pctl, off_clear, off_meta, off_queue, off_scr, total,
+  u64 off_err, off_cnt, off_acc, off_ev, off_ctl, off_pctl, off_clear, off_queue, off_scr, total,
       max_jobs, q_inst, scr_words, cnts, off_ztab, lmax;
   QueueTable Q;
 };
@@ -304,6 +338,8 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPl
   p->q_inst = total_inst;
   p->scr_words = (total_inst / 56 + 1) * 8ull * v.k;
   p->cnts = total_inst / 448 + 1;
+  // job records pack the merge bases as scratch word (40 bits) | counter << 40
+  if (p->scr_words >= (1ull << 40) || p->cnts >= (1ull << 24)) return fail(HTH_EINVAL, "varlen batch too large");
   u64 qcap = 0;
   for (int c = 0; c < NCLS; c++) {
     p->Q.qb[c] = qcap;
@@ -318,7 +354,6 @@ int varlen_plan(const VarInfo& v, u64 n, u64 total_bytes, u64 max_n_bytes, VarPl
   p->off_ctl = o; o += 256;
   p->off_pctl = o; o += 512;  // class counts [NCLS] u32 @0, scratch/counter totals @384
   p->off_clear = o;
-  p->off_meta = o; o = align_up(o + n * 16, 256);
   p->off_queue = o; o = align_up(o + qcap * 8 * JOB_REC, 256);
   p->off_scr = o; o = align_up(o + p->scr_words * 8, 256);
   p->off_ztab = o; o = align_up(o + ztab_base(p->lmax + 1, v.k) * 8, 256);
@@ -734,13 +769,20 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   int* err = (int*)(ws + p.off_err);
   u32* cls_cnt = (u32*)(ws + p.off_pctl);
   auto* totals = (unsigned long long*)(ws + p.off_pctl + 384);
-  // plan areas of an earlier call may overlap this call's counters/accumulators
-  CK(cudaMemsetAsync(ws, 0, p.off_clear, st));
+  int cur_dev = 0;
+  CK(cudaGetDevice(&cur_dev));
+  const WsSig sig{{p.off_cnt, p.off_acc, p.off_ev, p.off_ctl, p.off_pctl, p.off_clear, (u64)v.k, (u64)cur_dev}};
+  if (!ws_layout_known(ws, sig)) {
+    const cudaError_t e = cudaMemsetAsync(ws, 0, p.off_clear, st);
+    if (e != cudaSuccess) {
+      ws_forget(ws);
+      return cuda_fail(e, "cudaMemsetAsync(workspace)");
+    }
+  }
   const int job_lvl = pick_job_lvl(((max_n_bytes + 7) / 8) / (u64)v.m);
   int dev = 0;
   CK(cudaGetDevice(&dev));
   PlanParams Q{};
-  Q.data = (const uint8_t*)d_data;
   Q.off = d_offsets;
   Q.n = n_strings;
   Q.max_n = max_n_bytes;
@@ -748,30 +790,35 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   Q.job_lvl = job_lvl;
   Q.lmax = (u32)p.lmax;
   Q.S = d_seed;
+  Q.err = (int*)(ws + p.off_err);
+  Q.cls_cnt = cls_cnt;
+  Q.data = (const uint8_t*)d_data;
   Q.R = (u64)v.ew + 71ull * v.k;  // L' = 1 layout (hasher.py:130-153)
   Q.F0 = (u64)v.ew + 7ull * v.k;
   Q.out = d_out;
-  Q.err = (int*)(ws + p.off_err);
-  Q.cls_cnt = cls_cnt;
   Q.queues = (u64*)(ws + p.off_queue);
-  Q.meta = (u64*)(ws + p.off_meta);
   Q.totals = totals;
   Q.ztab = (u64*)(ws + p.off_ztab);
   Q.Q = p.Q;
-  const unsigned pb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 16), (u64)sm_count(dev) * 16));
-  if (int rc = by_width<PlanF>(output_bytes, Q, pb, st)) return rc;
+  // HTH_PLAN_SPW strings per warp, 8 warps per CTA (grid-stride beyond 8 CTAs per SM)
+  const unsigned pb = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(n_strings, 8 * HTH_PLAN_SPW), (u64)sm_count(dev) * 8));
+  if (int rc = by_width<PlanF>(output_bytes, Q, pb, st)) {
+    ws_forget(ws);
+    return rc;
+  }
   Params P{};
   P.data = (const uint8_t*)d_data;
   P.n_strings = n_strings;
   P.offsets = d_offsets;
   P.job_map = Q.queues;
-  P.meta = Q.meta;
   P.cls_cnt = cls_cnt;
+  P.totals = totals;
+  P.var_total = total_bytes;
   P.ztab = (const u64*)(ws + p.off_ztab);
   P.ztab_lmax = (u32)p.lmax;
   P.n_jobs = p.max_jobs;  // varlen: queue sizing bound; the kernel counts the jobs itself
   memcpy(P.cls_qb, p.Q.qb, sizeof(P.cls_qb));
-  P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_queue_kernel)
+  P.n_bytes = max_n_bytes;  // varlen: clamp bound (matches plan_kernel)
   P.S = d_seed;
   P.out = d_out;
   P.job_lvl = job_lvl;
@@ -781,16 +828,17 @@ int hth_hash_varlen(int output_bytes, const void* d_data, const uint64_t* d_offs
   P.acc = (u64*)(ws + p.off_acc);
   P.events = (u32*)(ws + p.off_ev);
   set_ctl(P, ws + p.off_ctl);
-  return dispatch<true>(output_bytes, P, p.max_jobs, st);
+  const int rc = dispatch<true>(output_bytes, P, p.max_jobs, st);
+  if (rc != HTH_OK) ws_forget(ws);  // the next call clears the workspace
+  return rc;
 }
 
 #ifdef HTH_DEBUG_TIMING
 // experiment builds only: copy and clear the per-warp timing records
 int hth_debug_timing(unsigned long long* host, int n_warps) {
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpyFromSymbol(host, hth_dbg, (size_t)n_warps * 10 * 8));
-  static unsigned long long zero[8192 * 10];
-  CK(cudaMemcpyToSymbol(hth_dbg, zero, sizeof(zero)));
+  CK(cudaMemcpy(host, dbg_buf(), (size_t)n_warps * 12 * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(dbg_buf(), 0, 8192 * 12 * 8));
   return HTH_OK;
 }
 #endif
@@ -799,6 +847,8 @@ int hth_varlen_status(void* d_workspace, void* stream) {
   int h = 0;
   CK(cudaMemcpyAsync(&h, d_workspace, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
+  // the flag accumulates over calls until read: clear what was reported
+  if (h) CK(cudaMemsetAsync(d_workspace, 0, 4, (cudaStream_t)stream));
   if (h & 1) return fail(HTH_ESEEDSIZE, "a string was longer than max_n_bytes; its digest is invalid");
   if (h & 4) return fail(HTH_EINVAL, "offsets decrease or run past total_bytes; digests are invalid");
   if (h & 2) return fail(HTH_EINVAL, "the strings hold more bytes than total_bytes declared; digests are invalid");
@@ -1170,6 +1220,7 @@ int hth_host_release(void) {
 int hth_workspace_reset(void* d_workspace, uint64_t workspace_bytes, void* stream) {
   if (!workspace_bytes) return HTH_OK;
   if (!d_workspace) return fail(HTH_EINVAL, "null workspace");
+  ws_forget(d_workspace);
   CK(cudaMemsetAsync(d_workspace, 0, workspace_bytes, (cudaStream_t)stream));
   return HTH_OK;
 }

@@ -15,7 +15,7 @@ namespace hth {
 
 #ifdef HTH_DEBUG_TIMING
 // experiment builds only: per warp {start, end, jobs, rounds, data-wait, valid, claim, decode, rounds, finish} (ns)
-__device__ unsigned long long hth_dbg[8192 * 10];
+// into P.dbg (8192 warps x 10)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -81,9 +81,10 @@ struct EhcSrc {
 
 // EHC leaf of two instances, lane j -> CA[r], CB[r] (hasher.py:356-364;
 // ehc.py:102-118).  offA/offB: word offset of lane j's first word of each
-// instance in the stage (instance base * m + j).
+// instance relative to its string's first byte, which sits at stage byte
+// dA / dB (the two instances may belong to different strings).
 template <int OUT, bool AL, class EH>
-__device__ __forceinline__ void leaf2o(const uint8_t* buf, u32 delta, u32 offA, u32 offB, const EH& P,
+__device__ __forceinline__ void leaf2o(const uint8_t* buf, u32 dA, u32 offA, u32 dB, u32 offB, const EH& P,
                                        u64 (&CA)[Var<OUT>::k], u64 (&CB)[Var<OUT>::k]) {
   using V = Var<OUT>;
   constexpr int K = V::k, E = V::e, D = V::d, WB = V::w, NP = E - D;
@@ -95,8 +96,8 @@ __device__ __forceinline__ void leaf2o(const uint8_t* buf, u32 delta, u32 offA, 
     w2 xa[D], xb[D];
 #pragma unroll
     for (int i = 0; i < D; i++) {
-      xa[i] = mk(ld_word<AL>(buf, delta, offA + (i * WB + u) * 8));
-      xb[i] = mk(ld_word<AL>(buf, delta, offB + (i * WB + u) * 8));
+      xa[i] = mk(ld_word<AL>(buf, dA, offA + (i * WB + u) * 8));
+      xb[i] = mk(ld_word<AL>(buf, dB, offB + (i * WB + u) * 8));
     }
     // hash the systematic items (ehc.py:49-72); seeds are constant-bank operands
 #pragma unroll
@@ -156,6 +157,12 @@ __device__ __forceinline__ void leaf2o(const uint8_t* buf, u32 delta, u32 offA, 
     CA[r] = a;
     CB[r] = b;
   }
+}
+
+template <int OUT, bool AL, class EH>
+__device__ __forceinline__ void leaf2o(const uint8_t* buf, u32 delta, u32 offA, u32 offB, const EH& P,
+                                       u64 (&CA)[Var<OUT>::k], u64 (&CB)[Var<OUT>::k]) {
+  leaf2o<OUT, AL>(buf, delta, offA, delta, offB, P, CA, CB);
 }
 
 // instances q and q+4 of an 8-instance round
@@ -248,6 +255,11 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   constexpr int K = V::k, M = Geo<V>::m;
   constexpr u32 CB = ROUND_INST * M * 8;  // stage payload bytes
   constexpr u32 SB = CB + 32;             // stage buffer: 16-B alignment superset + unaligned overread
+  // varlen pair jobs: Y's instances start here (X's <= 4 instances + 16 bytes of alignment before it)
+  constexpr u32 PAIR_OFF = 4 * M * 8 + 16;
+  static_assert(PAIR_OFF + 4 * M * 8 + 16 <= SB, "a pair's instances fit one stage");
+  constexpr u32 PAIR_MARK = 0xffffffffu;  // prem of a claimed, not yet issued pair job
+  constexpr u64 PAIR_BIT = 1ull << 63;    // record word 3 of a pair job (merge bases use < 64 bits)
   extern __shared__ __align__(128) uint8_t smem[];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -284,14 +296,19 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // cls_pre[0] = total jobs = end of class 1
   u32* cls_pre = reinterpret_cast<u32*>(smem + W * NS * SB + W * NS * 8 + W * NACC * 8 + W * QN * JOB_REC * 8 +
                                         (PS ? W * 2 * MAX_EW * 4 : 0));
+  u32* cls_raw = cls_pre + NCLS + 1;  // varlen: raw string counts of the pair classes
   u64 n_jobs = P.n_jobs;
   if (VARLEN) {
     // cls_pre[c] = jobs in classes > c (c >= 1), cls_pre[0] = all jobs: a
     // suffix scan of the 64 class counts by warp 0, two classes per lane
     static_assert(NCLS == 65, "two size classes per lane of one warp");
     if (warp == 0) {
+      // classes 1..PAIR_MAX: jobs are pairs of strings (two per round)
       const int c1 = 2 * lane + 1, c2 = c1 + 1;
-      const u32 a = P.cls_cnt[c1], b = P.cls_cnt[c2];
+      const u32 ra = P.cls_cnt[c1], rb = P.cls_cnt[c2];
+      if (c1 <= PAIR_MAX) cls_raw[c1] = ra;
+      if (c2 <= PAIR_MAX) cls_raw[c2] = rb;
+      const u32 a = c1 <= PAIR_MAX ? (ra + 1) >> 1 : ra, b = c2 <= PAIR_MAX ? (rb + 1) >> 1 : rb;
       u32 x = a + b;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -331,7 +348,22 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       if (cls_pre[mid] <= jc) hi = mid;
       else lo = mid + 1;
     }
-    const u64* q = P.job_map + (P.cls_qb[lo] + (jc - cls_pre[lo])) * JOB_REC;
+    const u64 li = jc - cls_pre[lo];
+    if (lo <= PAIR_MAX) {
+      // a pair job: strings 2 li and 2 li + 1 of the class ->
+      // {offset X, offset Y, sX | sY << 32, nX | nY << 32 | PAIR bit}
+      const u64* q = P.job_map + (P.cls_qb[lo] + 2 * li) * JOB_REC;
+      const bool hy = 2 * li + 1 < cls_raw[lo];
+      const u64 x0 = __ldg(q), x1 = __ldg(q + 1), x2 = __ldg(q + 2);
+      const u64 y0 = hy ? __ldg(q + JOB_REC) : 0, y1 = hy ? __ldg(q + JOB_REC + 1) : 0;
+      const u64 y2 = hy ? __ldg(q + JOB_REC + 2) : 0xffffffffull;
+      r1[0] = x0;
+      r1[1] = y0;
+      r1[2] = (x2 & 0xffffffffull) | (y2 << 32);
+      r1[3] = x1 | (y1 << 32) | PAIR_BIT;
+      return;
+    }
+    const u64* q = P.job_map + (P.cls_qb[lo] + li) * JOB_REC;
 #pragma unroll
     for (int i = 0; i < JOB_REC; i++) r1[i] = __ldg(q + i);
   };
@@ -362,6 +394,10 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
       e[0] = jc;
     }
     qhead++;
+    if (VARLEN && (r1[3] & PAIR_BIT)) {
+      prem = PAIR_MARK;  // p_issue_one copies both strings' instances into one stage
+      return true;
+    }
     Str st;
     u32 jq, ni;
     u64 b0;
@@ -384,6 +420,28 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
 #endif
   // hot path: one bulk copy per round, address advanced incrementally
   auto p_issue_one = [&]() {
+    if (VARLEN && prem == PAIR_MARK) {
+      // pair job (just claimed, the newest queue entry): X's instances at
+      // stage byte 0, Y's at PAIR_OFF, each as its 16-byte-aligned superset
+      const u32 slot = pseq % NS;
+      if (lane == 0) {
+        const u64* e = jq_buf + ((qhead - 1) % QN) * JOB_REC;
+        const u64 base = reinterpret_cast<u64>(P.data);
+        const u64 nX = e[3] & 0x7fffffffull, nY = (e[3] >> 32) & 0x7fffffffull;
+        const u64 aX = base + e[0], aY = base + e[1];
+        // instance bytes only, never past the string's last byte
+        const u64 iX = min(nX, (u64)((((nX + 7) >> 3) / M) * (M * 8ull)));
+        const u64 iY = min(nY, (u64)((((nY + 7) >> 3) / M) * (M * 8ull)));
+        const u32 lX = (u32)(((aX + iX + 15) & ~15ull) - (aX & ~15ull));
+        const u32 lY = nY ? (u32)(((aY + iY + 15) & ~15ull) - (aY & ~15ull)) : 0;
+        mbar_arrive_expect_tx(&bars[slot], lX + lY);
+        bulk_g2s(ring + slot * SB, reinterpret_cast<const void*>(aX & ~15ull), lX, &bars[slot], pol);
+        if (lY) bulk_g2s(ring + slot * SB + PAIR_OFF, reinterpret_cast<const void*>(aY & ~15ull), lY, &bars[slot], pol);
+      }
+      pseq++;
+      prem = 0;
+      return;
+    }
     const u32 len = min(CB, prem);
     const u64 a0 = psrc & ~15ull;
     const u32 bytes = (u32)(((psrc + len + 15) & ~15ull) - a0);
@@ -427,6 +485,79 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     __syncwarp();
     const u64* jrec = jq_buf + (qtail % QN) * JOB_REC;
     qtail++;
+    if constexpr (VARLEN) {
+      if (jrec[3] & PAIR_BIT) {
+        // Two one-level strings X, Y of <= 4 instances in one round: thread
+        // (q, j) computes lane j of instance q of each.  Every instance is a
+        // level-0 leftover (slot q, tree.py:103-134); the Toeplitz tails are
+        // read from global memory (hasher.py:407-412).
+        constexpr int EW = Geo<V>::ew;
+        constexpr int NP = 2 * K <= 4 ? 4 : (2 * K <= 8 ? 8 : 16);
+        const u64 oX = jrec[0], oY = jrec[1], sxy = jrec[2], nxy = jrec[3];
+        const u64 nX = nxy & 0x7fffffffull, nY = (nxy >> 32) & 0x7fffffffull;
+        const u64 sX = sxy & 0xffffffffull, sY = sxy >> 32;
+        const bool hasY = sY != 0xffffffffull;
+        const u32 cX = (u32)(((nX + 7) >> 3) / M), cY = hasY ? (u32)(((nY + 7) >> 3) / M) : 0;
+        const u64 base = reinterpret_cast<u64>(P.data);
+        const u32 dX = (u32)((base + oX) & 15), dY = (u32)((base + oY) & 15) + PAIR_OFF;
+        const u32 slot = cseq % NS;
+        mbar_wait(&bars[slot], (cseq / NS) & 1);
+        // a partial last word inside the instances (no tail): zero-pad it (hasher.py:179-183)
+        const bool padX = nX < (u64)cX * M * 8;  // then nX > cX * m * 8 - 8 and nX % 8 != 0
+        const bool padY = hasY && nY < (u64)cY * M * 8;
+        if (padX || padY) {
+          uint8_t* b = ring + slot * SB;
+          if (padX && (u32)lane < 8 - (u32)(nX & 7)) b[dX + nX + lane] = 0;
+          if (padY && (u32)lane < 8 - (u32)(nY & 7)) b[dY + nY + lane] = 0;
+          fence_proxy_async();
+          __syncwarp();
+        }
+        u64 CA[K], CB_[K];
+        leaf2o<OUT, false>(ring + slot * SB, dX, (u32)(q * M + j), dY, (u32)(q * M + j), eh, CA, CB_);
+        __syncwarp();
+        cseq++;
+        if (prem != 0 && pseq - cseq == (u32)NS - 1)
+          p_issue_one();
+        else
+          p_issue();
+        const u64 F1 = (u64)EW + 7ull * K, R1 = (u64)EW + 71ull * K;  // one-level layout (hasher.py:130-153)
+        u64 a[NP];
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          a[r] = (u32)q < cX ? nh_acc(0ull, CA[r], sd(F1 + 64ull * r + q * 8 + j)) : 0;
+          a[K + r] = (u32)q < cY ? nh_acc(0ull, CB_[r], sd(F1 + 64ull * r + q * 8 + j)) : 0;
+        }
+#pragma unroll
+        for (int r = 2 * K; r < NP; r++) a[r] = 0;
+        const u64 tX = (u64)cX * M, tY = (u64)cY * M;
+        const u64 nwX = (nX + 7) >> 3, nwY = hasY ? (nY + 7) >> 3 : 0;
+        for (u64 t = tX + lane; t < nwX; t += 32) {
+          const u64 y = gword(P.data, oX, nX, t);
+#pragma unroll
+          for (int r = 0; r < K; r++) a[r] = nh_acc(a[r], y, sd(R1 + r + (t - tX)));
+        }
+        for (u64 t = tY + lane; t < nwY; t += 32) {
+          const u64 y = gword(P.data, oY, nY, t);
+#pragma unroll
+          for (int r = 0; r < K; r++) a[K + r] = nh_acc(a[K + r], y, sd(R1 + r + (t - tY)));
+        }
+        if (lane == 0) {
+          // zero slots cX..6 and the length tag (tree.py:103-134)
+#pragma unroll
+          for (int r = 0; r < K; r++) {
+            a[r] = nh_acc(a[r] + P.ztab[cX * K + r], nX, sd(F1 + 64ull * r + 56));
+            if (hasY) a[K + r] = nh_acc(a[K + r] + P.ztab[cY * K + r], nY, sd(F1 + 64ull * r + 56));
+          }
+        }
+        const u64 tot = warp_reduce_scatter<NP>(a, lane);
+        const int idx = warp_scatter_index<NP>(lane);
+        if ((lane & (32 / NP - 1)) == 0) {
+          if (idx < K) P.out[sX * K + idx] = tot;
+          else if (idx < 2 * K && hasY) P.out[sY * K + idx - K] = tot;
+        }
+        continue;
+      }
+    }
     Str st;
     u32 jq, ninst;
     u64 byte0, nbytes;
@@ -689,11 +820,14 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
 #endif
   }
 #ifdef HTH_DEBUG_TIMING
+  const unsigned long long dbg_jobs_end = gtimer();
+#endif
+#ifdef HTH_DEBUG_TIMING
   if (lane == 0) {
     const u64 gw = (u64)blockIdx.x * W + warp;
     if (gw < 8192) {
-      unsigned long long* d = hth_dbg + gw * 10;
-      d[0] = dbg_t0; d[1] = gtimer(); d[2] = dbg_jobs; d[3] = dbg_rounds; d[4] = dbg_wait; d[5] = 1;
+      unsigned long long* d = P.dbg + gw * 12;
+      d[0] = dbg_t0; d[1] = gtimer(); d[2] = dbg_jobs; d[3] = dbg_rounds; d[4] = dbg_wait; d[5] = dbg_jobs_end;
       d[6] = dbg_claim; d[7] = dbg_dec; d[8] = dbg_loop; d[9] = dbg_fin;
     }
   }
@@ -707,11 +841,16 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // and, exchanging in-stream, publishes the slice: every warp fenced its
   // peer stores (fence.sc.sys above) before its arrival, so a fence and a
   // release store by the last arriver order them all before the flag
-  if ((claims || P.done_flag) && lane == 0) {
+  if ((claims || P.done_flag || VARLEN) && lane == 0) {
     const u32 old = atomicAdd(P.exit_ctr, 1u);
     if (old + 1 == gridDim.x * (u32)W) {
       *P.job_ctr = 0;
       *P.exit_ctr = 0;
+      if (VARLEN) {  // every CTA read the plan's counts at its start: leave them zeroed for the next call
+        for (int c = 0; c < NCLS; c++) P.cls_cnt[c] = 0;
+        P.totals[0] = 0;
+        P.totals[1] = 0;
+      }
       if (P.done_flag) {
         __threadfence_system();
         st_release_sys(P.done_flag, P.done_value);

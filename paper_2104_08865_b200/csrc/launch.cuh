@@ -166,7 +166,7 @@ int VarEngine<OUT>::small(const Params& P, cudaStream_t st) {
 }
 template <int OUT>
 int VarEngine<OUT>::plan(const PlanParams& Q, unsigned grid, cudaStream_t st) {
-  plan_tail_kernel<OUT><<<grid, 256, 0, st>>>(Q);
+  plan_kernel<OUT><<<grid, 256, 0, st>>>(Q);
   CK(cudaGetLastError());
   return HTH_OK;
 }

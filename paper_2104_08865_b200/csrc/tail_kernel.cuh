@@ -27,50 +27,6 @@ struct TailParams {
   u64 tag[5];  // NH(n, S[F_r]) per output word
 };
 
-// Sum v[0..K) over the 16 lanes of each half-warp; afterwards lane g holds
-// the total of word (g & (KP-1)) for g < KP (KP = K rounded up to 2^n).
-template <int K>
-__device__ __forceinline__ u64 half_reduce_scatter(u64 (&v)[K], int g) {
-  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
-  u64 a[KP];
-#pragma unroll
-  for (int r = 0; r < KP; r++) a[r] = r < K ? v[r] : 0;
-  // step with mask 8 (and 4 when KP == 8): halve the live words per lane
-  int live = KP;
-#pragma unroll
-  for (int m = 8; m >= 1; m >>= 1) {
-    if (live > 1) {
-      const int half = live / 2;
-      const bool upper = (g & m) != 0;  // keep upper half of the live words
-#pragma unroll
-      for (int r = 0; r < KP / 2; r++) {
-        if (r < half) {
-          const u64 send = upper ? a[r] : a[r + half];
-          const u64 keep = upper ? a[r + half] : a[r];
-          a[r] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-        }
-      }
-      live = half;
-    } else {
-      a[0] += __shfl_xor_sync(0xffffffffu, a[0], m);
-    }
-  }
-  return a[0];
-}
-
-// lane g ends with the word index it holds after half_reduce_scatter
-template <int K>
-__device__ __forceinline__ int scatter_index(int g) {
-  constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
-  int idx = 0, live = KP;
-  for (int m = 8; m >= 1 && live > 1; m >>= 1) {
-    const int half = live / 2;
-    if (g & m) idx += half;
-    live = half;
-  }
-  return idx;
-}
-
 // Per warp: a ring of NS stages, each one cp.async.bulk copy of GP PAIRS of
 // consecutive strings (2 GP x stride bytes), so the loads stay deep in flight
 // without holding registers and each copy is large enough to stream at full

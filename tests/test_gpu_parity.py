@@ -228,6 +228,34 @@ def test_varlen_every_length_up_to_ten_instances(hh, w):
     assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]}"
 
 
+@pytest.mark.parametrize("w", VARIANTS)
+@pytest.mark.parametrize("odd", (0, 1))
+def test_varlen_pairs_and_small_last_jobs(hh, w, odd):
+    # one-level strings of 1..4 instances are hashed two per round (pair
+    # jobs, any tail length, an odd count per class leaves one unpaired);
+    # multi-job strings whose last job holds 1..4 instances (64 k + 1..4, and
+    # 512 + 1..4 / 4096 + 1..4 with 512-instance jobs) must not be paired
+    from workloads import offsets_of
+
+    iw = o.variant(w).m * 8
+    rng = np.random.default_rng(100 * w + odd)
+    small = [c * iw + int(rng.integers(0, iw)) for c in range(1, 5) for _ in range(7 + 2 * c + odd)]
+    multi = [(64 * k + c) * iw + int(rng.integers(0, iw)) for k in (1, 2) for c in range(1, 5)]
+    if odd:
+        multi += [(4096 + c) * iw + 5 for c in (1, 4)]  # 512-instance jobs
+    lengths = rng.permutation(np.array(small + multi + [0, 1, iw - 1], dtype=np.int64))
+    off = offsets_of(lengths)
+    total = int(off[-1])
+    buf = hh.fill_bytes(total, 44 + odd)
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, int(lengths.max()))
+    got = _u64(hh.hash_varlen(buf, off, seed, p))
+    host = np.frombuffer(o.fill_bytes(total, 44 + odd), dtype=np.uint8).copy()
+    want = coracle.hash_varlen(w, host, off, seed.words_np(0, seed.capacity))
+    bad = np.nonzero(~np.all(got == want, axis=1))[0]
+    assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]}"
+
+
 @pytest.mark.parametrize("n_strings", (16384, 16385, 70001))
 def test_varlen_plan_paths(hh, n_strings):
     # up to 16384 strings are planned by one block (plan_one_kernel), more by

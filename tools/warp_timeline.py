@@ -19,7 +19,7 @@ wk = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 lib = _lib.lib()
 lib.hth_debug_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
 NW = 8192
-rec = np.zeros((NW, 10), dtype=np.uint64)
+rec = np.zeros((NW, 12), dtype=np.uint64)
 
 
 def run():
@@ -46,7 +46,7 @@ for _ in range(3):
 lib.hth_debug_timing(rec.ctypes.data, NW)
 f()
 lib.hth_debug_timing(rec.ctypes.data, NW)
-r = rec[rec[:, 5] == 1].astype(np.float64)
+r = rec[rec[:, 5] != 0].astype(np.float64)
 t0 = r[:, 0].min()
 st, en = (r[:, 0] - t0) / 1e3, (r[:, 1] - t0) / 1e3
 busy = en - st
@@ -56,6 +56,9 @@ print(f"{wk}: {len(r)} warps; span {en.max():.1f} us; warp start spread {st.min(
 print(f"jobs/warp mean {r[:, 2].mean():.2f} max {r[:, 2].max():.0f}; rounds/warp mean {r[:, 3].mean():.1f} "
       f"max {r[:, 3].max():.0f}; data-wait share of warp time {r[:, 4].sum() / 1e3 / busy.sum():.1%}; "
       f"warp-time utilisation (sum busy / (warps x span)) {busy.sum() / (len(r) * en.max()):.1%}")
+je = (r[:, 5] - t0) / 1e3
+print(f"job phase end p10/p50/p90/max {np.percentile(je, 10):.1f}/{np.percentile(je, 50):.1f}/{np.percentile(je, 90):.1f}/"
+      f"{je.max():.1f} us (then exit)")
 print(f"mean us per round (busy / rounds) {busy.sum() / r[:, 3].sum():.2f}")
 J = r[:, 2].sum()
 idle = busy.sum() - (r[:, 7].sum() + r[:, 8].sum() + r[:, 9].sum()) / 1e3
