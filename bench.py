@@ -52,7 +52,7 @@ UNIT = "GB/s"
 # the dominant kernel of each workload (launch configuration picked by the C-ABI)
 KERNELS = {
     "cfg1": "small_kernel<24, G=1, W=2, NS=2, MINB=4> (one launch per step)",
-    "cfg2": "per variant: plan_tail_kernel<w> + hash_kernel<w, varlen> (4 variants on 4 streams, one CUDA graph)",
+    "cfg2": "per variant: plan_kernel<w> + hash_kernel<w, varlen> (4 variants on 4 streams, one CUDA graph)",
     "cfg3": "tail_kernel<32, CPT=4, unmasked, NS=1, GP=4> (one launch per step)",
     "cfg4": "hash_kernel<40, fixed, W=2, NS=2, MINB=5, AL8> (one launch per step)",
     "cfg5": "hash_kernel<16, fixed, W=4, NS=2, MINB=4, AL8> (one launch per step)",
@@ -363,7 +363,8 @@ def make_flush(torch):
 def measure_latency(hh, sizes=(64, 4096, 1 << 20, 64 << 20), variant=24, reps=20):
     """Single-string latency of the public one-shot API (hash_bytes on host
     bytes: seed expansion, H2D copy, hash, digest read-back),
-    wall clock, median of `reps` calls, beside the CPU port on one core."""
+    wall clock, median of 500 calls (inputs up to 64 KiB) or `reps` calls,
+    beside the CPU port on one core."""
     from oracle import oracle_np as o
 
     p = hh.variant(variant)
@@ -372,10 +373,11 @@ def measure_latency(hh, sizes=(64, 4096, 1 << 20, 64 << 20), variant=24, reps=20
     for n in sizes:
         data = wl.host_bytes(0, n)
         seed = hh.seed_for_input(wl.MASTER, p, n)
-        for _ in range(3):
+        small = n <= 1 << 16
+        for _ in range(50 if small else 3):
             d = hh.hash_bytes(data, seed, p)
         ts = []
-        for _ in range(reps):
+        for _ in range(500 if small else reps):
             t0 = time.perf_counter()
             d = hh.hash_bytes(data, seed, p)
             ts.append(time.perf_counter() - t0)
@@ -465,9 +467,10 @@ def measure_workload(hh, torch, workload, steps, warmup, peak, barrier=None):
                    l2="flushed (256 MB write) before every timed step",
                    execution="4 variants on 4 forked streams, captured as one CUDA graph, replayed per step",
                    graph_matches_serial=same,
-                   bound=("latency: ~10 us fixed per variant call (workspace clear + planning kernel + hash "
-                          "kernel launch) and ~3 us per warp job (claim, decode, finalize) against ~2.5 us "
-                          "rounds; 98 MB per variant is 15 us of HBM time (DESIGN.md section 5)"))
+                   bound=("latency: per variant two launches (plan kernel, which also hashes the ~10k strings "
+                          "shorter than one instance, then the job kernel) and ~3 us per warp job (claim, "
+                          "decode, finalize) against 2-3 us unaligned rounds; 98 MB per variant is 15 us of HBM "
+                          "time (DESIGN.md section 5)"))
         del buf
         return res
     ctx = setup_fixed(hh, torch, workload)
@@ -484,9 +487,28 @@ def measure_workload(hh, torch, workload, steps, warmup, peak, barrier=None):
         res["bound"] = ("latency: one launch hashes 4 MiB (0.6 us of HBM time); each warp's critical path is "
                         "one stage's DRAM round trip after the flush + one two-instance leaf + finalize "
                         "(profiles/README.md)")
+        floor = _cfg1_floor()
+        if floor:
+            res["floor"] = floor
+            res["frac_of_floor"] = floor["us"] / (ms * 1e3)
     del ctx
     torch.cuda.empty_cache()
     return res
+
+
+def _cfg1_floor():
+    """Config 1's measured floor (tools/peaks.cu, committed): 1024 warps each
+    doing one 4 KiB bulk copy + one 24-byte store after the same 256 MB L2
+    flush, CUDA events around the launch -- everything but the hash."""
+    path = os.path.join(ROOT, "profiles", "peaks_r02.json")
+    try:
+        with open(path) as fh:
+            f = json.load(fh)["cfg1_floor_us"]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"us": f["bulk_copy_4KiB_per_warp"], "empty_launch_us": f["empty_launch"],
+            "what": "512 CTAs x 2 warps: one 4 KiB cp.async.bulk + one 24-byte store per warp after the L2 flush, "
+                    "event-timed like the step", "source": "profiles/peaks_r02.json (tools/peaks.cu)"}
 
 
 def e2e_fixed(hh, torch, workload, steps, n_strings_cap=None, rank=0, world=1, local_rank=0, dist=None):

@@ -189,6 +189,8 @@ def _check_capacity(seed: SeedBuffer, params: HashParams, n_bytes: int) -> None:
             "expand with seed_words_needed()")
 
 
+_OUT_T = {k: ctypes.c_uint64 * k for k in (2, 3, 4, 5)}  # digest words per variant
+
 #: engine names accepted by hash_bytes: the GPU engine, and the reference's
 #: two engine names as aliases of it (identical digests)
 ENGINES = ("cuda", "lanes", "scalar")
@@ -222,13 +224,15 @@ def hash_bytes(data, seed: SeedBuffer, params: HashParams, engine: str = "cuda",
         _check_capacity(seed, params, n)
         out = hash_fixed(data.reshape(1, n), n, seed, params)
         return Digest(tuple(int(x) for x in out.cpu().numpy().view(np.uint64)[0]))
-    buf = bytes(data)
-    _check_capacity(seed, params, len(buf))
-    out = (ctypes.c_uint64 * k)()
+    buf = data if type(data) is bytes else bytes(data)
+    out = _OUT_T[k]()
     dev = 0 if device is None else int(device)
-    _lib.check(_lib.lib().hth_hash_host(params.output_bytes, buf, len(buf), seed.master, seed.capacity,
-                                        out, dev))
-    return Digest(tuple(int(x) for x in out))
+    # the C-ABI checks the seed capacity itself (HTH_ESEEDSIZE -> SeedSizeError,
+    # hasher.py:209-214), so the host path is a single foreign call
+    rc = _lib.lib().hth_hash_host(params.output_bytes, buf, len(buf), seed.master, seed.capacity, out, dev)
+    if rc:
+        _lib.check(rc)
+    return Digest(tuple(out))
 
 
 def digest(data, master: bytes = b"\x00" * 32, output_bytes: int = 24) -> Digest:
