@@ -20,7 +20,7 @@ for c in $CFGS; do
 done
 if [ "$1" = B ]; then
   python tools/exp_varlen.py 40 > /dev/null 2>&1 || exit 1
-  ncu --set full --clock-control none --import-source on -k "regex:hash_kernel|plan_tail" -c 2 \
+  ncu --set full --clock-control none --import-source on -k "regex:hash_kernel|plan_kernel" -c 2 \
     -o gpurun_out/${T}_cfg2v40 python tools/exp_varlen.py 40 > gpurun_out/${T}_cfg2.log 2>&1
 fi
 ls -la gpurun_out/
