@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   // varlen pair jobs: Y's instances start here (X's <= 4 instances + 16 bytes of alignment before it)
   constexpr u32 PAIR_OFF = 4 * M * 8 + 16;
   static_assert(PAIR_OFF + 4 * M * 8 + 16 <= SB, "a pair's instances fit one stage");
+  // strings of <= 3 instances (< 4 m * 8 bytes with their tail) fit whole
+  constexpr bool PAIR_FULL = PAIR_MAX <= 3;
   constexpr u32 PAIR_MARK = 0xffffffffu;  // prem of a claimed, not yet issued pair job
   constexpr u64 PAIR_BIT = 1ull << 63;    // record word 3 of a pair job (merge bases use < 64 bits)
   extern __shared__ __align__(128) uint8_t smem[];
@@ -423,15 +425,17 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
     if (VARLEN && prem == PAIR_MARK) {
       // pair job (just claimed, the newest queue entry): X's instances at
       // stage byte 0, Y's at PAIR_OFF, each as its 16-byte-aligned superset
+      // (PAIR_FULL: the whole strings, tails included)
       const u32 slot = pseq % NS;
       if (lane == 0) {
         const u64* e = jq_buf + ((qhead - 1) % QN) * JOB_REC;
         const u64 base = reinterpret_cast<u64>(P.data);
         const u64 nX = e[3] & 0x7fffffffull, nY = (e[3] >> 32) & 0x7fffffffull;
         const u64 aX = base + e[0], aY = base + e[1];
-        // instance bytes only, never past the string's last byte
-        const u64 iX = min(nX, (u64)((((nX + 7) >> 3) / M) * (M * 8ull)));
-        const u64 iY = min(nY, (u64)((((nY + 7) >> 3) / M) * (M * 8ull)));
+        // PAIR_FULL: whole strings (instances + tail, < 4 m * 8 bytes each);
+        // else instance bytes only; never past the string's last byte
+        const u64 iX = PAIR_FULL ? nX : min(nX, (u64)((((nX + 7) >> 3) / M) * (M * 8ull)));
+        const u64 iY = PAIR_FULL ? nY : min(nY, (u64)((((nY + 7) >> 3) / M) * (M * 8ull)));
         const u32 lX = (u32)(((aX + iX + 15) & ~15ull) - (aX & ~15ull));
         const u32 lY = nY ? (u32)(((aY + iY + 15) & ~15ull) - (aY & ~15ull)) : 0;
         mbar_arrive_expect_tx(&bars[slot], lX + lY);
@@ -502,9 +506,10 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
         const u32 dX = (u32)((base + oX) & 15), dY = (u32)((base + oY) & 15) + PAIR_OFF;
         const u32 slot = cseq % NS;
         mbar_wait(&bars[slot], (cseq / NS) & 1);
-        // a partial last word inside the instances (no tail): zero-pad it (hasher.py:179-183)
-        const bool padX = nX < (u64)cX * M * 8;  // then nX > cX * m * 8 - 8 and nX % 8 != 0
-        const bool padY = hasY && nY < (u64)cY * M * 8;
+        // zero-pad a partial last word in the stage (hasher.py:179-183): the
+        // string's last word (PAIR_FULL), else only one inside the instances
+        const bool padX = PAIR_FULL ? (nX & 7) != 0 : nX < (u64)cX * M * 8;
+        const bool padY = hasY && (PAIR_FULL ? (nY & 7) != 0 : nY < (u64)cY * M * 8);
         if (padX || padY) {
           uint8_t* b = ring + slot * SB;
           if (padX && (u32)lane < 8 - (u32)(nX & 7)) b[dX + nX + lane] = 0;
@@ -513,13 +518,16 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
           __syncwarp();
         }
         u64 CA[K], CB_[K];
-        leaf2o<OUT, false>(ring + slot * SB, dX, (u32)(q * M + j), dY, (u32)(q * M + j), eh, CA, CB_);
-        __syncwarp();
-        cseq++;
-        if (prem != 0 && pseq - cseq == (u32)NS - 1)
-          p_issue_one();
-        else
-          p_issue();
+        const uint8_t* pbuf = ring + slot * SB;
+        leaf2o<OUT, false>(pbuf, dX, (u32)(q * M + j), dY, (u32)(q * M + j), eh, CA, CB_);
+        if (!PAIR_FULL) {  // the stage is consumed; the tails come from global memory
+          __syncwarp();
+          cseq++;
+          if (prem != 0 && pseq - cseq == (u32)NS - 1)
+            p_issue_one();
+          else
+            p_issue();
+        }
         const u64 F1 = (u64)EW + 7ull * K, R1 = (u64)EW + 71ull * K;  // one-level layout (hasher.py:130-153)
         u64 a[NP];
 #pragma unroll
@@ -532,14 +540,22 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
         const u64 tX = (u64)cX * M, tY = (u64)cY * M;
         const u64 nwX = (nX + 7) >> 3, nwY = hasY ? (nY + 7) >> 3 : 0;
         for (u64 t = tX + lane; t < nwX; t += 32) {
-          const u64 y = gword(P.data, oX, nX, t);
+          const u64 y = PAIR_FULL ? ld_word<false>(pbuf, dX, (u32)t) : gword(P.data, oX, nX, t);
 #pragma unroll
           for (int r = 0; r < K; r++) a[r] = nh_acc(a[r], y, sd(R1 + r + (t - tX)));
         }
         for (u64 t = tY + lane; t < nwY; t += 32) {
-          const u64 y = gword(P.data, oY, nY, t);
+          const u64 y = PAIR_FULL ? ld_word<false>(pbuf, dY, (u32)t) : gword(P.data, oY, nY, t);
 #pragma unroll
           for (int r = 0; r < K; r++) a[K + r] = nh_acc(a[K + r], y, sd(R1 + r + (t - tY)));
+        }
+        if (PAIR_FULL) {  // tails read: the stage is consumed
+          __syncwarp();
+          cseq++;
+          if (prem != 0 && pseq - cseq == (u32)NS - 1)
+            p_issue_one();
+          else
+            p_issue();
         }
         if (lane == 0) {
           // zero slots cX..6 and the length tag (tree.py:103-134)
