@@ -496,6 +496,27 @@ def measure_workload(hh, torch, workload, steps, warmup, peak, barrier=None):
     return res
 
 
+# exact NH multiplies per input byte (entropy_report of the
+# reference's analysis.py:241-248 on each config)
+MULT_PER_BYTE = {"cfg1": 0.2058, "cfg2": 0.300, "cfg3": 0.5039, "cfg4": 0.2676, "cfg5": 0.1667}
+
+
+def _imad_bound(workload, achieved_gbs):
+    """The north-star's other roofline: the 32x32->64 multiply pipe.  Rate =
+    the measured IMAD.WIDE.U32 issue rate (tools/peaks.cu, profiles/peaks_r02.json)
+    at the attribute clock; bound = rate / NH multiplies per byte."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_r02.json")) as fh:
+            tops = json.load(fh)["imad_wide_tops"]
+    except (OSError, KeyError, ValueError):
+        return None
+    mpb = MULT_PER_BYTE[workload]
+    bound = tops * 1e12 / mpb / 1e9
+    return {"mult_per_byte": mpb, "imad_wide_tops": tops, "bound_gbs": bound, "frac": achieved_gbs / bound,
+            "note": "multiply-pipe roofline (measured IMAD.WIDE.U32 rate / multiplies per byte): never the "
+                    "binding one here; the HBM figure is"}
+
+
 def _cfg1_floor():
     """Config 1's measured floor (tools/peaks.cu, committed): 1024 warps each
     doing one 4 KiB bulk copy + one 24-byte store after the same 256 MB L2
@@ -966,7 +987,8 @@ def arm_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(workload),
                          "kernel": KERNELS[workload], "kernel_ms": kernel_ms,
-                         "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
+                         "algorithmic_bytes_per_launch": algo, "peak_source": peak_src,
+                         "imad": _imad_bound(workload, achieved)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * (8 if workload == "cfg2" else 1),
