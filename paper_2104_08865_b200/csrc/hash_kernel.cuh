@@ -342,14 +342,18 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
 #endif
   // varlen: job id -> its record in the class queues (one global load)
   u64 r1[JOB_REC];
-  auto v_fetch = [&](u64 jc) {
-    // the smallest class c with cls_pre[c] <= jc (cls_pre falls as c grows)
+  // the smallest class c with cls_pre[c] <= jc (cls_pre falls as c grows)
+  auto v_class = [&](u64 jc) -> int {
     int lo = 1, hi = NCLS - 1;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (cls_pre[mid] <= jc) hi = mid;
       else lo = mid + 1;
     }
+    return lo;
+  };
+  auto v_fetch = [&](u64 jc) {
+    const int lo = v_class(jc);
     const u64 li = jc - cls_pre[lo];
     if (lo <= PAIR_MAX) {
       // a pair job: strings 2 li and 2 li + 1 of the class ->
