@@ -301,6 +301,9 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
   u32* cls_raw = cls_pre + NCLS + 1;  // varlen: raw string counts of the pair classes
   u64 n_jobs = P.n_jobs;
   if (VARLEN) {
+    // launched as a programmatic dependent of the plan kernel: wait for its
+    // completion (and memory) before reading what it planned
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // cls_pre[c] = jobs in classes > c (c >= 1), cls_pre[0] = all jobs: a
     // suffix scan of the 64 class counts by warp 0, two classes per lane
     static_assert(NCLS == 65, "two size classes per lane of one warp");

@@ -5,6 +5,10 @@
 #pragma once
 #include "engine_api.cuh"
 
+#ifndef HTH_VARLEN_PDL
+#define HTH_VARLEN_PDL 1
+#endif
+
 namespace hth {
 
 // ------------------------------------------------------------ launch config
@@ -49,6 +53,23 @@ int launch_hash(const Params& P, u64 n_jobs_bound, cudaStream_t st) {
   const u64 need = ceil_div(n_jobs_bound, W);
   if (need < grid) grid = need;
   if (grid == 0) grid = 1;
+  if (VARLEN && HTH_VARLEN_PDL) {
+    // programmatic dependent launch: the CTAs start (mbarrier setup) while
+    // the plan kernel finishes and wait for its results in-kernel
+    // (griddepcontrol.wait before the class counts are read)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(W * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, P));
+    return HTH_OK;
+  }
   kern<<<(unsigned)grid, W * 32, smem, st>>>(P);
   CK(cudaGetLastError());
   return HTH_OK;

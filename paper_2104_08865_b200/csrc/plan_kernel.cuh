@@ -28,6 +28,9 @@ namespace hth {
 #ifndef HTH_PLAN_MINB
 #define HTH_PLAN_MINB 4
 #endif
+#ifndef HTH_PLAN_TRIGGER_EARLY
+#define HTH_PLAN_TRIGGER_EARLY 0
+#endif
 struct QueueTable {
   u64 qb[NCLS + 1];  // queue c occupies job_map[qb[c], qb[c+1])
 };
@@ -78,6 +81,11 @@ __global__ void __launch_bounds__(256, HTH_PLAN_MINB) plan_kernel(const __grid_c
   static_assert(SPW >= 1 && SPW <= 32, "strings per warp");
   __shared__ u64 key[M + K - 1];  // Toeplitz keys R .. R + m + k - 2 (the end of the L' = 1 layout)
   __shared__ u64 tagseed[K];
+#if HTH_PLAN_TRIGGER_EARLY
+  // let the hash kernel (a programmatic dependent) start its prologue now;
+  // it waits for this grid's completion before reading the plan
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
   const int lane = threadIdx.x & 31;
   const u64 gwarp = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
@@ -227,6 +235,12 @@ __global__ void __launch_bounds__(256, HTH_PLAN_MINB) plan_kernel(const __grid_c
       if (ok && (g & (16 / KP - 1)) == 0 && myidx < K) P.out[(base + my) * K + myidx] = tot;
     }
   }
+#if !HTH_PLAN_TRIGGER_EARLY
+  // this CTA is done: once every CTA got here the hash kernel (a
+  // programmatic dependent) may start its prologue; it waits for this
+  // grid's completion and memory before reading the plan
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
 }
 
 }  // namespace hth
