@@ -256,6 +256,36 @@ def test_varlen_pairs_and_small_last_jobs(hh, w, odd):
     assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]}"
 
 
+def test_varlen_workspace_reused_across_layouts(hh):
+    # one workspace, alternating batch shapes: the engine clears its counter
+    # region only when the layout changes and otherwise relies on the
+    # kernels leaving it zeroed -- every call must still match the oracle
+    import torch
+
+    from paper_2104_08865_b200 import batch
+    from workloads import offsets_of
+
+    w = 32
+    p = hh.variant(w)
+    rng = np.random.default_rng(77)
+    shapes = [rng.integers(0, 9000, 300), rng.integers(0, 3000, 1100), rng.integers(0, 80000, 40)]
+    bufs = []
+    for i, ln in enumerate(shapes):
+        ln = ln.astype(np.int64)
+        off = offsets_of(ln)
+        total = int(off[-1])
+        bufs.append((hh.fill_bytes(total, 60 + i), off, total, int(ln.max())))
+    wsz = max(batch.workspace_varlen(p, len(o_) - 1, t) for _, o_, t, _ in bufs)
+    ws = torch.zeros(wsz, dtype=torch.uint8, device="cuda")
+    for k in (0, 1, 0, 2, 2, 1, 0):
+        buf, off, total, mx = bufs[k]
+        seed = hh.seed_for_input(bytes(range(32)), p, mx)
+        got = _u64(hh.hash_varlen(buf, off, seed, p, workspace=ws))
+        host = np.frombuffer(o.fill_bytes(total, 60 + k), dtype=np.uint8).copy()
+        want = coracle.hash_varlen(w, host, off, seed.words_np(0, seed.capacity))
+        assert np.array_equal(got, want), k
+
+
 @pytest.mark.parametrize("n_strings", (16384, 16385, 70001))
 def test_varlen_plan_paths(hh, n_strings):
     # up to 16384 strings are planned by one block (plan_one_kernel), more by
