@@ -812,29 +812,32 @@ __global__ void __launch_bounds__(W * 32, MINB) hash_kernel(const __grid_constan
         for (int r = 0; r < K; r++) fin[r] = nh_acc(fin[r], st.n, sd(tc.F(r)));
       }
     }
-    u64 mine = 0;
+    // the k row sums over the warp, scattered (one 32-lane reduce-scatter:
+    // 9 shuffles for k = 5 instead of 25): `own` lanes hold row `row`
+    constexpr int NPK = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
+    u64 rs[NPK];
 #pragma unroll
-    for (int r = 0; r < K; r++) {
-      const u64 v = warp_sum(fin[r]);
-      if (lane == r) mine = v;
-    }
+    for (int r = 0; r < NPK; r++) rs[r] = r < K ? fin[r] : 0;
+    const u64 mine = warp_reduce_scatter<NPK>(rs, lane);
+    const int row = warp_scatter_index<NPK>(lane);
+    const bool own = (lane & (32 / NPK - 1)) == 0 && row < K;
     if (P.frontier_lvl) {
       // slice mode: accumulate only; the merge step publishes the digest
-      if (lane < K && mine) atomicAdd(reinterpret_cast<unsigned long long*>(P.acc) + lane, (unsigned long long)mine);
+      if (own && mine) atomicAdd(reinterpret_cast<unsigned long long*>(P.acc) + row, (unsigned long long)mine);
     } else if (st.J == 1) {
-      if (lane < K) P.out[st.s * K + lane] = mine;
+      if (own) P.out[st.s * K + row] = mine;
     } else if (events) {
       // multi-job string: add this job's finalize terms, then count its
       // events; the warp completing the count publishes the digest and
       // re-zeroes the accumulators (integer sums: order-independent).
       unsigned long long* a = reinterpret_cast<unsigned long long*>(P.acc + st.s * K);
-      if (lane < K) atomicAdd(a + lane, (unsigned long long)mine);
+      if (own) atomicAdd(a + row, (unsigned long long)mine);
       __syncwarp();
       u32 old = 0;
       if (lane == 0) old = atom_add_acq_rel(P.events + st.s, events);
       old = __shfl_sync(0xffffffffu, old, 0);
       if (old + events == string_events(st.n_inst, job_lvl)) {
-        if (lane < K) P.out[st.s * K + lane] = atomicExch(a + lane, 0ull);
+        if (own) P.out[st.s * K + row] = atomicExch(a + row, 0ull);
         if (lane == 0) P.events[st.s] = 0;
       }
     }
