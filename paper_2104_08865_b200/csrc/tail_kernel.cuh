@@ -14,6 +14,10 @@
 #pragma once
 #include "engine.cuh"
 
+#ifndef HTH_TAIL_MINB
+#define HTH_TAIL_MINB 2
+#endif
+
 namespace hth {
 
 struct TailParams {
@@ -32,7 +36,7 @@ struct TailParams {
 // without holding registers and each copy is large enough to stream at full
 // HBM rate.  MASKED: n % 16 != 0 (partial words / chunks).
 template <int OUT, int CPT, bool MASKED, int NS, int GP>
-__global__ void __launch_bounds__(256, 2) tail_kernel(const __grid_constant__ TailParams P) {
+__global__ void __launch_bounds__(256, HTH_TAIL_MINB) tail_kernel(const __grid_constant__ TailParams P) {
   constexpr int K = Var<OUT>::k;
   constexpr int KP = K <= 2 ? 2 : (K <= 4 ? 4 : 8);
   extern __shared__ __align__(128) uint8_t smem[];
