@@ -935,7 +935,7 @@ def arm_ours(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1:
         if not args.no_extra:
-            for wk in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
+            for wk in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "probe_tail1296"):
                 if wk == workload:
                     continue
                 try:

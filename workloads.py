@@ -28,6 +28,11 @@ CONFIGS = {
     "cfg3": dict(desc="4,194,304 x 1024 B (4 GiB), v32", variant=32, n_strings=4 * 1024 * 1024, n_bytes=1024),
     "cfg4": dict(desc="8192 x 1 MiB (8 GiB), v40", variant=40, n_strings=8192, n_bytes=1 << 20),
     "cfg5": dict(desc="1 x 16 GiB, v16", variant=16, n_strings=1, n_bytes=16 << 30),
+    # not a BASELINE config: a probe of the masked six-chunks-per-lane tail
+    # kernel (strings of 81 16-byte chunks), the path whose register spills
+    # were removed in round 2
+    "probe_tail1296": dict(desc="probe: 3,000,000 x 1296 B (3.9 GB), v32, masked 6-chunk tail kernel", variant=32,
+                           n_strings=3_000_000, n_bytes=1296),
 }
 
 
