@@ -480,8 +480,10 @@ def measure_workload(hh, torch, workload, steps, warmup, peak, barrier=None):
     ms = total_ms / steps
     algo = _algo_bytes(workload, ctx["B"], ctx["n"], k)
     gbs = ctx["B"] * ctx["n"] / (ms / 1e3) / 1e9
+    rp = _read_peak(algo / (ms / 1e3) / 1e9)
     res.update(value=gbs, ms_per_step=ms, bytes_per_step=ctx["B"] * ctx["n"],
                roofline_frac=(algo / (ms / 1e3) / 1e9) / peak,
+               frac_of_read_peak=rp["frac"] if rp else None,
                l2="flushed before every timed step" if flush else "inputs larger than L2 (126 MB)")
     if workload == "cfg1":
         res["bound"] = ("latency: one launch hashes 4 MiB (0.6 us of HBM time); each warp's critical path is "
@@ -515,6 +517,19 @@ def _imad_bound(workload, achieved_gbs):
     return {"mult_per_byte": mpb, "imad_wide_tops": tops, "bound_gbs": bound, "frac": achieved_gbs / bound,
             "note": "multiply-pipe roofline (measured IMAD.WIDE.U32 rate / multiplies per byte): never the "
                     "binding one here; the HBM figure is"}
+
+
+def _read_peak(achieved_gbs):
+    """The kernels only read HBM (digests are ~0.01 % of the bytes), so beside
+    the contract's copy peak (read + write) report the measured read-only
+    streaming peak of their own load path: TMA bulk copies into a per-warp
+    ring, best of a stage-size x warps/SM sweep (tools/peaks.cu)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_r02.json")) as fh:
+            rd = json.load(fh)["tma_read_gbs"]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"gbs": rd, "frac": achieved_gbs / rd, "source": "profiles/peaks_r02.json tma_read_gbs (tools/peaks.cu)"}
 
 
 def _cfg1_floor():
@@ -988,7 +1003,7 @@ def arm_ours(args, rank, world, local_rank):
                          "frac": achieved / peak, "traffic": _traffic(workload),
                          "kernel": KERNELS[workload], "kernel_ms": kernel_ms,
                          "algorithmic_bytes_per_launch": algo, "peak_source": peak_src,
-                         "imad": _imad_bound(workload, achieved)},
+                         "imad": _imad_bound(workload, achieved), "read_peak": _read_peak(achieved)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * (8 if workload == "cfg2" else 1),
