@@ -519,6 +519,18 @@ def _imad_bound(workload, achieved_gbs):
                     "binding one here; the HBM figure is"}
 
 
+def _cpu_model():
+    """The host CPU the CPU baseline ran on (state the model)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def _read_peak(achieved_gbs):
     """The kernels only read HBM (digests are ~0.01 % of the bytes), so beside
     the contract's copy peak (read + write) report the measured read-only
@@ -612,7 +624,8 @@ def arm_reference(args, rank, world):
         "data": "synthetic (splitmix stream, seed 0)",
         "config": {"workload": workload, "desc": cfg["desc"], "variant": cfg["variant"],
                    "bytes_per_step": tot},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": cpu.kind, "sample": cpu.sample()},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": cpu.kind, "sample": cpu.sample(),
+                         "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -986,7 +999,7 @@ def arm_ours(args, rank, world, local_rank):
             c1.close()
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": cb.kind,
                "sample": cb.sample() + f"; median of {len(runs)} passes, {sum(x[2] for x in runs):.2f} s",
-               "single_core_value": r1}
+               "single_core_value": r1, "cpu_model": _cpu_model()}
     if rank == 0:
         cfg = wl.CONFIGS[workload]
         line = {
