@@ -375,7 +375,7 @@ struct Params {
   u64 cnt_per;   // fixed mode: counters per string
   const u64* offsets;  // varlen: n_strings + 1 byte offsets
   const u64* job_map;  // varlen: per-size-class job queues; each job a JOB_REC-word record
-                       // {byte offset, length, string | job index << 32, 0} (plan_tail_kernel)
+                       // {byte offset, length, string | job index << 32, merge bases} (plan_kernel)
   u32* cls_cnt;        // varlen: jobs per size class (plan_kernel; reset at exit)
   unsigned long long* totals;  // varlen: the plan's scratch/counter allocators (reset at exit)
   u64 var_total;       // varlen: data bytes (offset bound)
@@ -444,7 +444,7 @@ __device__ __forceinline__ void decode_job(const Params& P, u64 job, const u64* 
   if (VARLEN) {
     s = rec[2] & 0xffffffffull;
     st.p = P.data + rec[0];
-    st.n = rec[1];  // clamped to the host-checked bound by plan_tail_kernel
+    st.n = rec[1];  // clamped to the host-checked bound by plan_kernel
     jq = (u32)(rec[2] >> 32);
   } else {
     // jq-major order: all strings' first jobs, then all second jobs, ...

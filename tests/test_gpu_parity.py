@@ -288,8 +288,8 @@ def test_varlen_workspace_reused_across_layouts(hh):
 
 @pytest.mark.parametrize("n_strings", (16384, 16385, 70001))
 def test_varlen_plan_paths(hh, n_strings):
-    # up to 16384 strings are planned by one block (plan_one_kernel), more by
-    # the count / device-scan / scatter kernels; both must give the same digests
+    # batch sizes around and far beyond one planning pass, with a few
+    # multi-job strings among them: every string must come back hashed
     from workloads import offsets_of
 
     rng = np.random.default_rng(n_strings)
