@@ -300,10 +300,14 @@ struct FixedPlan {
   int job_lvl;
 };
 // frontier > 0: slice mode, merges stop below that level
+// Few long strings (fewer than kLvl3Jobs level-3 jobs in the batch) use
+// level-2 jobs instead, so a single 1 MiB string is 18 warps' work, not 3.
+constexpr u64 kLvl3Jobs = 4096;
 FixedPlan fixed_plan(const VarInfo& v, u64 n_strings, u64 n_bytes, int frontier = 0) {
   FixedPlan f;
   f.n_inst = ((n_bytes + 7) / 8) / (u64)v.m;
   f.job_lvl = pick_job_lvl(f.n_inst);
+  if (frontier == 0 && f.job_lvl == 3 && n_strings * job_count(f.n_inst, 3) < kLvl3Jobs) f.job_lvl = 2;
   f.J = job_count(f.n_inst, f.job_lvl);
   f.n_jobs = n_strings * f.J;
   scratch_need(f.n_inst, v.k, f.job_lvl, &f.scr_per, &f.cnt_per, frontier > 0 ? frontier : 64);
@@ -519,7 +523,11 @@ int h2d(HostCtx* c, void* dst, const void* src, u64 bytes, cudaStream_t st) {
   cudaPointerAttributes a{};
   const bool pinned = cudaPointerGetAttributes(&a, src) == cudaSuccess && a.type != cudaMemoryTypeUnregistered;
   cudaGetLastError();  // clear a sticky error from the attribute query on plain pointers
-  if (pinned || bytes < (8ull << 20)) {
+  static const u64 direct_below = [] {
+    const char* e = getenv("HTH_PAGEABLE_DIRECT");  // experiments: pageable sizes left to the driver
+    return e ? strtoull(e, nullptr, 10) : (256ull << 10);
+  }();
+  if (pinned || bytes < direct_below) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     return HTH_OK;
   }
@@ -529,10 +537,17 @@ int h2d(HostCtx* c, void* dst, const void* src, u64 bytes, cudaStream_t st) {
       CK(cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
     }
   }
+  // slices of about a quarter of the copy (256 KiB .. one slot), so even a
+  // few-MiB input overlaps its memcpy with its DMA
+  static const u64 min_slice = [] {
+    const char* e = getenv("HTH_RING_MIN_SLICE");  // experiments
+    return e ? strtoull(e, nullptr, 10) : (256ull << 10);
+  }();
+  const u64 slice = std::min<u64>(kRing, std::max<u64>(min_slice, ((bytes / 4) + 63) & ~63ull));
   u64 i = 0;
-  for (u64 off = 0; off < bytes; off += kRing, i++) {
+  for (u64 off = 0; off < bytes; off += slice, i++) {
     const int slot = (int)(i & 1);
-    const u64 len = std::min(kRing, bytes - off);
+    const u64 len = std::min(slice, bytes - off);
     CK(cudaEventSynchronize(c->ring_ev[slot]));  // the slot's previous DMA has drained
     par_memcpy(c->ring[slot], (const uint8_t*)src + off, len);
     CK(cudaMemcpyAsync((uint8_t*)dst + off, c->ring[slot], len, cudaMemcpyHostToDevice, st));
