@@ -9,7 +9,7 @@ import paper_2104_08865_b200 as hh  # noqa: E402
 
 p = hh.variant(24)
 out = {}
-for n in (300 << 10, 1 << 20, 4 << 20, 8 << 20, 16 << 20):
+for n in (300 << 10, 1 << 20, 4 << 20, 8 << 20, 16 << 20, 64 << 20):
     data = os.urandom(n)
     seed = hh.seed_for_input(bytes(range(32)), p, n)
     for _ in range(10):
