@@ -41,3 +41,17 @@ def test_bench_rejects_world_size_mismatch():
     r = _run(["--gpus", "2", "--impl", "reference"], env={"WORLD_SIZE": "3", "RANK": "0"})
     assert r.returncode == 2
     assert "WORLD_SIZE=3" in r.stderr
+
+
+def test_bench_roofline_helpers():
+    # the bench line's secondary rooflines come from committed measurements
+    sys.path.insert(0, ROOT)
+    import bench
+
+    imad = bench._imad_bound("cfg4", 6100.0)
+    assert imad and imad["bound_gbs"] > 10 * 6100.0  # the multiply pipe never binds here
+    rp = bench._read_peak(6100.0)
+    assert rp and 0 < rp["frac"] < 1.2
+    floor = bench._cfg1_floor()
+    assert floor and 0 < floor["empty_launch_us"] < floor["us"]
+    assert set(bench.MULT_PER_BYTE) >= {"cfg1", "cfg2", "cfg3", "cfg4", "cfg5"}
