@@ -817,3 +817,54 @@ def test_stream_hasher_matches_one_shot(hh, w):
         h.digest()
     with pytest.raises(ValueError):
         h.update(b"123456")
+
+
+def test_cuda_graph_replays(hh):
+    # one captured sequence (a multi-job fixed batch whose counters and
+    # accumulators self-reset, then a varlen batch: planner + job kernel as a
+    # programmatic dependent), replayed several times on the same workspaces:
+    # every replay must reproduce the oracle digests
+    import torch
+
+    from paper_2104_08865_b200 import batch
+    from workloads import offsets_of
+
+    w = 40
+    p = hh.variant(w)
+    n, B = 1100 * o.variant(w).m * 8 + 13, 5  # 1,100 instances: level-2 jobs with merges
+    fbuf = hh.fill_bytes(B * n, 70)
+    fseed = hh.seed_for_input(bytes(range(32)), p, n)
+    fws = torch.zeros(batch.workspace_fixed(p, B, n), dtype=torch.uint8, device="cuda")
+    fout = torch.empty((B, p.output_words), dtype=torch.int64, device="cuda")
+    lengths = np.random.default_rng(71).integers(0, 70000, 500).astype(np.int64)
+    off = offsets_of(lengths)
+    total = int(off[-1])
+    vbuf = hh.fill_bytes(total, 72)
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    vseed = hh.seed_for_input(bytes(range(32)), p, int(lengths.max()))
+    vws = torch.zeros(batch.workspace_varlen(p, len(lengths), total), dtype=torch.uint8, device="cuda")
+    vout = torch.empty((len(lengths), p.output_words), dtype=torch.int64, device="cuda")
+
+    def step():
+        hh.hash_fixed(fbuf, n, fseed, p, n_strings=B, stride=n, out=fout, workspace=fws)
+        hh.hash_varlen(vbuf, d_off, vseed, p, max_n_bytes=int(lengths.max()), out=vout, workspace=vws, check=False)
+
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        step()  # warm-up outside capture (first-layout workspace clear)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step()
+    fwant = coracle.hash_fixed(w, np.frombuffer(o.fill_bytes(B * n, 70), dtype=np.uint8).copy(), B, n, n,
+                               fseed.words_np(0, fseed.capacity))
+    vwant = coracle.hash_varlen(w, np.frombuffer(o.fill_bytes(total, 72), dtype=np.uint8).copy(), off,
+                                vseed.words_np(0, vseed.capacity))
+    for _ in range(3):
+        fout.zero_()
+        vout.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(_u64(fout), fwant)
+        assert np.array_equal(_u64(vout), vwant)
+    batch.varlen_status(vws)
