@@ -868,3 +868,46 @@ def test_cuda_graph_replays(hh):
         assert np.array_equal(_u64(fout), fwant)
         assert np.array_equal(_u64(vout), vwant)
     batch.varlen_status(vws)
+
+
+@pytest.mark.parametrize("n_strings", (2047, 2048))
+def test_job_level_threshold(hh, n_strings):
+    # 600-instance strings: 2047 of them make 4094 level-3 jobs (the batch
+    # runs level-2 jobs), 2048 make 4096 (level-3 jobs); digests must agree
+    # with the oracle either way
+    w = 16
+    v = o.variant(w)
+    n = 600 * v.m * 8 + 5
+    stride = n + 11
+    buf = hh.fill_bytes(n_strings * stride, 80)
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, n)
+    got = _u64(hh.hash_fixed(buf, n, seed, p, n_strings=n_strings, stride=stride))
+    host = np.frombuffer(o.fill_bytes(n_strings * stride, 80), dtype=np.uint8).copy()
+    want = coracle.hash_fixed(w, host, n_strings, stride, n, seed.words_np(0, seed.capacity))
+    assert np.array_equal(got, want)
+
+
+def test_varlen_many_pair_jobs_dynamic_claims(hh):
+    # thousands of one-level strings of 1-4 instances (pair jobs, claimed
+    # dynamically), odd counts per class, random tails and alignments, mixed
+    # with multi-job strings whose last job is small (class 5)
+    from workloads import offsets_of
+
+    w = 24
+    iw = o.variant(w).m * 8
+    rng = np.random.default_rng(90)
+    c = rng.integers(1, 5, 6001)
+    lengths = c * iw + rng.integers(0, iw, c.size)
+    multi = (64 * rng.integers(1, 3, 41) + rng.integers(1, 5, 41)) * iw + rng.integers(0, iw, 41)
+    lengths = rng.permutation(np.concatenate([lengths, multi, rng.integers(0, iw, 300)]).astype(np.int64))
+    off = offsets_of(lengths)
+    total = int(off[-1])
+    buf = hh.fill_bytes(total, 91)
+    p = hh.variant(w)
+    seed = hh.seed_for_input(bytes(range(32)), p, int(lengths.max()))
+    got = _u64(hh.hash_varlen(buf, off, seed, p))
+    host = np.frombuffer(o.fill_bytes(total, 91), dtype=np.uint8).copy()
+    want = coracle.hash_varlen(w, host, off, seed.words_np(0, seed.capacity))
+    bad = np.nonzero(~np.all(got == want, axis=1))[0]
+    assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]}"
