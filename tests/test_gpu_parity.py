@@ -703,14 +703,17 @@ def test_host_api_strides_and_capacity(hh):
 
 
 def test_host_paths_pageable_staging_and_small_calls(hh):
-    # the three host-copy routes of hth_hash_fixed_host: <= 256 KiB calls via
-    # pinned staging on one stream, pageable inputs >= 8 MiB via the parallel
-    # memcpy into pinned slots (several slots, a partial last one), pinned
-    # sources straight to the DMA engine -- all equal to the oracle
+    # the host-copy routes of hth_hash_fixed_host: <= 64 KiB calls read
+    # mapped pinned memory, <= 256 KiB go through pinned staging on one
+    # stream, larger pageable inputs through the parallel memcpy into pinned
+    # slots (quarter-size slices from 256 KiB, 16 MiB slots for large ones, a
+    # partial last slice), pinned sources straight to the DMA engine -- all
+    # equal to the oracle
     import torch
 
     master = bytes(range(32))
-    for w, n in ((24, 100), (40, 200_000), (16, (40 << 20) + 13), (40, (33 << 20) + 5)):
+    for w, n in ((24, 100), (40, 200_000), (32, 300_001), (24, (1 << 20) + 3), (40, (5 << 20) + 77),
+                 (16, (40 << 20) + 13), (40, (33 << 20) + 5)):
         p = hh.variant(w)
         data = o.fill_bytes(n, 11)
         S = o.splitmix_words(o.master_fold(master), 0, o.seed_words_needed(o.variant(w), n))
