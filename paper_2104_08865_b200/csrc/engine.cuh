@@ -104,15 +104,6 @@ __device__ __forceinline__ u64 mac_const(u64 acc, u64 h) {
   return acc + h * (u64)C;
 }
 
-// x * v on 16 bit-sliced GF(16) elements (gf16.py:17-21), in 32-bit halves:
-// lo = planes 0,1; hi = planes 2,3.  2 PRMT + 1 LOP3.
-__device__ __forceinline__ w2 xtime(w2 v) {
-  u32 nlo = __byte_perm(v.hi, v.lo, 0x5432);  // (lo << 16) | (hi >> 16)
-  u32 nhi = __byte_perm(v.lo, v.hi, 0x5432);  // (hi << 16) | (lo >> 16)
-  nlo ^= v.hi & 0xFFFF0000u;                  // reduction x^4 = x + 1
-  return {nlo, nhi};
-}
-
 // Arrival on a merge/completion counter: release publishes this warp's
 // prior stores (ordered before lane 0 by __syncwarp), acquire makes the
 // other warps' blocks visible to a last arriver.  Lowers to MEMBAR.ALL.GPU
@@ -153,11 +144,6 @@ __device__ __forceinline__ bool wait_geq_sys(const unsigned long long* p, u64 v,
 template <class T>
 __device__ __forceinline__ T shfl_xor(T v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
-}
-__device__ __forceinline__ u64 warp_sum(u64 v) {
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-  return v;
 }
 
 // Sum v[0..K) over the 16 lanes of each half-warp; afterwards lane g holds
