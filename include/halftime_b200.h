@@ -94,6 +94,14 @@ int hth_master_fold(const uint8_t master[32], uint64_t* fold);
  * d_words[i] = mix(fold + (start + i + 1) * 0x9E3779B97F4A7C15). */
 int hth_expand_seed(uint64_t fold, uint64_t start, uint64_t count, uint64_t* d_words, void* stream);
 
+/* hash_remainder (hasher.py:186-206) on the device, for callers of the
+ * reference's component API: d_out[r] = sum_{i<n} NH(d_tail[i],
+ * d_keys[r + i]) for r < k (32-bit halves, the Toeplitz windows of the
+ * remainder region).  HTH_EINVAL ("remainder key region too short") when
+ * n_keys < n + k - 1, as the reference raises ValueError. */
+int hth_toeplitz_nh(const uint64_t* d_tail, uint64_t n, const uint64_t* d_keys, uint64_t n_keys, int k,
+                    uint64_t* d_out, void* stream);
+
 /* cli.fill_bytes (cli.py:48-53) on the device: n_bytes of the splitmix stream
  * keyed by fill_seed, starting at stream word `word_offset`. */
 int hth_fill_splitmix(uint64_t fill_seed, uint64_t word_offset, uint64_t n_bytes, void* d_dst, void* stream);

@@ -26,7 +26,7 @@ EXPORTS = (
     "hth_slice_plan", "hth_workspace_size_slice", "hth_hash_slice", "hth_hash_merge", "hth_hash_fixed_folds",
     "hth_ipc_get_handle", "hth_ipc_open_handle", "hth_ipc_close_handle", "hth_host_release",
     "hth_workspace_reset", "hth_hash_slice_ex", "hth_hash_merge_ex", "hth_signal", "hth_wait_flag",
-    "hth_fill_splitmix_strings",
+    "hth_fill_splitmix_strings", "hth_toeplitz_nh",
 )
 
 HTH_SLICE_ACCUMULATE = 1
@@ -85,6 +85,7 @@ def lib() -> ctypes.CDLL:
             "hth_signal": [vp, u64, vp],
             "hth_wait_flag": [vp, u64, u64, vp, vp],
             "hth_fill_splitmix_strings": [u64, u64, u64, u64, u64, vp, u64, vp],
+            "hth_toeplitz_nh": [vp, u64, vp, u64, i32, vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)

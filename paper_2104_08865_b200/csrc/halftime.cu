@@ -178,6 +178,24 @@ __global__ void expand_seed_kernel(u64 fold, u64 start, u64 count, u64* out) {
     out[i] = mix64(fold + (start + i + 1) * 0x9E3779B97F4A7C15ull);
 }
 
+// hash_remainder (hasher.py:186-206): one CTA per output row r, the block
+// sums NH(tail[i], keys[r + i]) over i.
+__global__ void toeplitz_nh_kernel(const u64* tail, u64 n, const u64* keys, u64* out) {
+  __shared__ u64 part[32];
+  const u64 r = blockIdx.x;
+  u64 acc = 0;
+  for (u64 i = threadIdx.x; i < n; i += blockDim.x) acc = nh_acc(acc, tail[i], keys[r + i]);
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
+    out[r] = t;
+  }
+}
+
 // Publish / await one flag in-stream (system scope; see wait_geq_sys).
 __global__ void signal_kernel(unsigned long long* flag, u64 value) {
   __threadfence_system();
@@ -617,6 +635,17 @@ int hth_expand_seed(uint64_t fold, uint64_t start, uint64_t count, uint64_t* d_w
   if (!d_words) return fail(HTH_EINVAL, "null seed buffer");
   const u64 blocks = std::min<u64>(ceil_div(count, 256), 4096);
   expand_seed_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(fold, start, count, d_words);
+  CK(cudaGetLastError());
+  return HTH_OK;
+}
+
+int hth_toeplitz_nh(const uint64_t* d_tail, uint64_t n, const uint64_t* d_keys, uint64_t n_keys, int k,
+                    uint64_t* d_out, void* stream) {
+  if (k < 0) return fail(HTH_EINVAL, "k must be >= 0");
+  if (n_keys + 1 < n + (u64)k) return fail(HTH_EINVAL, "remainder key region too short");
+  if (!k) return HTH_OK;
+  if (!d_out || (n && (!d_tail || !d_keys))) return fail(HTH_EINVAL, "null device pointer");
+  toeplitz_nh_kernel<<<(unsigned)k, 256, 0, (cudaStream_t)stream>>>(d_tail, n, d_keys, d_out);
   CK(cudaGetLastError());
   return HTH_OK;
 }

@@ -41,6 +41,7 @@ MASK64 = (1 << 64) - 1
 __all__ = [
     "Digest", "SeedBuffer", "SeedLayout", "SeedSizeError", "digest", "expand_seed", "hash_bytes",
     "seed_for_input", "seed_layout", "seed_words_needed", "instance_count", "splitmix_mix", "ENGINES",
+    "words_from_bytes", "hash_remainder",
 ]
 
 
@@ -147,6 +148,45 @@ def _check_params(params: HashParams) -> HashParams:
 
 def instance_count(params: HashParams, n_bytes: int) -> int:
     return ((n_bytes + 7) // 8) // params.instance_words
+
+
+def words_from_bytes(data: bytes) -> list:
+    """Little-endian 64-bit words, the final partial word zero-padded
+    (hasher.py:179-183): the word view every engine hashes."""
+    data = bytes(data)
+    if len(data) % 8:
+        data += b"\x00" * (8 - len(data) % 8)
+    return [int(x) for x in np.frombuffer(data, dtype="<u8")]
+
+
+def hash_remainder(tail, remainder_words, k: int, half_bits: int = 32, counter=None) -> tuple:
+    """The Toeplitz remainder (hasher.py:186-206) on the GPU: component i is
+    NH of ``tail`` under ``remainder_words[i : i + len(tail)]``.
+
+    As ``hash_bytes``, the GPU engine keeps no multiplication counter
+    (``counter`` raises ``ValueError``) and works on 32-bit halves only.
+    """
+    if counter is not None:
+        raise ValueError("multiplication counting is not available on the GPU engine")
+    if half_bits != 32:
+        raise ValueError("the GPU engine hashes 32-bit halves (half_bits=32)")
+    n, k = len(tail), int(k)
+    if len(remainder_words) < n + k - 1:
+        raise ValueError("remainder key region too short")
+    if k <= 0:
+        return ()
+    if n == 0:
+        return (0,) * k
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    as_dev = lambda v: torch.from_numpy(np.asarray(v, dtype=np.uint64).view(np.int64).copy()).to(dev)
+    t, keys = as_dev(list(tail)), as_dev(list(remainder_words))
+    out = torch.empty(k, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().hth_toeplitz_nh(t.data_ptr(), n, keys.data_ptr(), keys.numel(), k, out.data_ptr(),
+                                              torch.cuda.current_stream(dev).cuda_stream))
+    return tuple(int(x) for x in out.cpu().numpy().view(np.uint64))
 
 
 def seed_layout(params: HashParams, n_bytes: int) -> SeedLayout:

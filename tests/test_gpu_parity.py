@@ -914,3 +914,25 @@ def test_varlen_many_pair_jobs_dynamic_claims(hh):
     want = coracle.hash_varlen(w, host, off, seed.words_np(0, seed.capacity))
     bad = np.nonzero(~np.all(got == want, axis=1))[0]
     assert bad.size == 0, f"{bad.size} mismatches; lengths {lengths[bad[:8]]}"
+
+
+def test_hash_remainder_on_the_gpu(hh):
+    # hash_remainder (hasher.py:186-206): component i is NH of the tail under
+    # the key window starting at i (pkg/tests/test_hasher.py:187-211)
+    from paper_2104_08865_b200.hasher import hash_remainder
+
+    M64 = (1 << 64) - 1
+
+    def nh(x, s):
+        return (((x + s) & 0xFFFFFFFF) * (((x >> 32) + (s >> 32)) & 0xFFFFFFFF)) & M64
+
+    rng = np.random.default_rng(5)
+    for n, k in ((1, 1), (7, 3), (300, 5), (1001, 2)):
+        tail = [int(x) for x in rng.integers(0, 1 << 63, n, dtype=np.uint64) * 2 + 1]
+        keys = [int(x) for x in rng.integers(0, 1 << 63, n + k + 3, dtype=np.uint64) * 3]
+        want = tuple(sum(nh(tail[j], keys[i + j]) for j in range(n)) & M64 for i in range(k))
+        assert hash_remainder(tail, keys, k) == want, (n, k)
+    # the windows overlap: component i+1 of keys == component i of keys[1:]
+    tail, keys = [5, 6, 7], [11, 12, 13, 14, 15]
+    a, b = hash_remainder(tail, keys, 3), hash_remainder(tail, keys[1:], 2)
+    assert a[1:] == b

@@ -141,3 +141,18 @@ def test_engine_names_checked_before_gpu_work():
         hh.hash_bytes(b"", s, p, engine="neon")
     with pytest.raises(ValueError):
         hh.hash_bytes(b"", s, p, engine="lanes", counter=object())
+
+
+def test_words_from_bytes_and_remainder_errors():
+    # pkg/tests/test_hasher.py:153-155, 187-188 (no GPU work for these cases)
+    from paper_2104_08865_b200.hasher import hash_remainder, words_from_bytes
+
+    assert words_from_bytes(b"\x01\x00\x00\x00\x00\x00\x00\x00\xff") == [1, 255]
+    assert words_from_bytes(b"") == []
+    assert hash_remainder([], [1, 2, 3], k=3) == (0, 0, 0)
+    with pytest.raises(ValueError):
+        hash_remainder([1, 2, 3], [1, 2, 3], k=2)  # key region too short
+    with pytest.raises(ValueError):
+        hash_remainder([1], [1, 2], k=1, counter=object())
+    with pytest.raises(ValueError):
+        hash_remainder([1], [1, 2], k=1, half_bits=16)
