@@ -574,7 +574,19 @@ def e2e_fixed(hh, torch, workload, steps, n_strings_cap=None, rank=0, world=1, l
         hh.fill_bytes(B * n, wl.DATA_SEED, rank * B * n // 8, out=dev)
     else:
         dev = ctx["buf"]
-    host = torch.empty(B * n, dtype=torch.uint8, pin_memory=True)
+    # every rank pins its buffer before any collective, and all ranks agree
+    # on success, so a rank that cannot pin never leaves the others waiting
+    try:
+        host = torch.empty(B * n, dtype=torch.uint8, pin_memory=True)
+        ok = 1
+    except Exception:  # pragma: no cover
+        host, ok = None, 0
+    if dist:
+        f = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(f, op=dist.ReduceOp.MIN)
+        ok = int(f.item())
+    if not ok:
+        raise RuntimeError("could not pin the e2e host buffer on every rank")
     host.copy_(dev[:B * n])
     del dev, ctx
     torch.cuda.empty_cache()
@@ -942,8 +954,10 @@ def arm_ours(args, rank, world, local_rank):
     e2e = None
     if args.e2e_steps > 0 and workload != "cfg2":
         try:
-            e2e, e2e_out = e2e_fixed(hh, torch, workload, args.e2e_steps, args.e2e_strings, rank, world, local_rank,
-                                     dist)
+            # N > 1: 2 GiB per rank (the e2e figure is a rate; 8 ranks x 8 GiB of
+            # pinned host memory is more than a box need offer)
+            e2e_cap = args.e2e_strings or (2048 if world > 1 and workload == "cfg4" else 0)
+            e2e, e2e_out = e2e_fixed(hh, torch, workload, args.e2e_steps, e2e_cap, rank, world, local_rank, dist)
             if rank == 0 and not args.no_check:  # the host-path digests of 4 strings against the oracle
                 from oracle import c as coracle
 
@@ -951,7 +965,7 @@ def arm_ours(args, rank, world, local_rank):
                 n_ = cfg["n_bytes"]
                 # rank 0's strings: global i (capped batch) or i * world (round-robin shard)
                 nchk = min(4, len(e2e_out))
-                gidx = [i if args.e2e_strings else i * world for i in range(nchk)]
+                gidx = [i if e2e_cap else i * world for i in range(nchk)]
                 host = _stream_strings(gidx, n_)
                 seed_ = hh.seed_for_input(wl.MASTER, hh.variant(cfg["variant"]), n_)
                 want = coracle.hash_fixed(cfg["variant"], host, nchk, n_, n_, seed_.words_np(0, seed_.capacity))
